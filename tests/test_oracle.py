@@ -1,0 +1,153 @@
+"""Pins for oracle/ (CPU only): the oracle is checked against things other than itself.
+
+* hand-computed cases (tests/golden/hand_cases.json, each cited);
+* math.fsum brute force of the exact fp64 products at sampled outputs;
+* torch.nn.functional.conv2d in float64 on CPU (an independent library
+  cross-correlation routine);
+* invariants on integer-valued data (where every fp64 sum is exact, so they
+  must hold bit-exactly): linearity, delta kernel = shifted input, shift
+  equivariance, C-additivity, zero weights, batch independence, output-channel
+  permutation.
+
+A dropped term, wrong sign, flipped kernel, swapped c/c' index or off-by-one
+bound in oracle/conv_oracle.c fails at least one of these.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hand_cases.json")
+
+
+def _int_data(shape, seed, lo=-8, hi=8):
+    rng = np.random.default_rng(seed)
+    return rng.integers(lo, hi + 1, size=shape).astype(np.float32)
+
+
+def test_hand_cases():
+    cases = json.load(open(GOLDEN))["cases"]
+    assert len(cases) >= 5
+    for case in cases:
+        I = np.asarray(case["I"], dtype=np.float32)
+        W = np.asarray(case["W"], dtype=np.float32)
+        O = oracle.conv_fp64(I, W)
+        np.testing.assert_array_equal(O, np.asarray(case["O"], dtype=np.float64), err_msg=case["name"])
+
+
+def test_flipped_kernel_differs():
+    # true convolution (kernel flip) would give [[23,33],[53,63]] for the orientation case
+    I = np.arange(1, 10, dtype=np.float32).reshape(1, 1, 3, 3)
+    W = np.array([[[[1, 2], [3, 4]]]], dtype=np.float32)
+    O = oracle.conv_fp64(I, W)
+    assert not np.array_equal(O[0, 0], np.array([[23, 33], [53, 63]], dtype=np.float64))
+
+
+@pytest.mark.parametrize("shape", [(2, 5, 3, 9, 11, 3), (1, 7, 2, 12, 8, 5), (3, 2, 4, 6, 6, 1)])
+def test_fsum_bruteforce(shape):
+    B, C, Co, H, Wd, r = shape
+    g = torch.Generator().manual_seed(7)
+    I = (torch.rand(B, C, H, Wd, generator=g) * 2 - 1).numpy()
+    W = (torch.rand(Co, C, r, r, generator=g) * 2 - 1).numpy()
+    O = oracle.conv_fp64(I, W)
+    Ho, Wo = H - r + 1, Wd - r + 1
+    rng = np.random.default_rng(3)
+    for _ in range(60):
+        b, co, i, j = rng.integers(B), rng.integers(Co), rng.integers(Ho), rng.integers(Wo)
+        terms = [float(I[b, c, i + p, j + q]) * float(W[co, c, p, q])
+                 for c in range(C) for p in range(r) for q in range(r)]
+        exact = math.fsum(terms)  # correctly rounded exact sum (products are exact in fp64)
+        scale = max(abs(t) for t in terms) or 1.0
+        assert abs(O[b, co, i, j] - exact) <= 1e-13 * scale * len(terms)
+    # corners too (ragged borders)
+    for (i, j) in ((0, 0), (0, Wo - 1), (Ho - 1, 0), (Ho - 1, Wo - 1)):
+        terms = [float(I[B - 1, c, i + p, j + q]) * float(W[Co - 1, c, p, q])
+                 for c in range(C) for p in range(r) for q in range(r)]
+        assert abs(O[B - 1, Co - 1, i, j] - math.fsum(terms)) <= 1e-13 * len(terms)
+
+
+def test_sampled_equals_full():
+    cfg = synth.custom(2, 6, 5, 13, 10, 3, seed=11)
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    idx = synth.sample_output_indices(cfg, 200, seed=5)
+    s = oracle.conv_fp64_sampled(I, W, idx)
+    np.testing.assert_array_equal(s, O[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]])
+
+
+@pytest.mark.parametrize("name", ["tiny", "small_r5", "rect"])
+def test_torch_conv2d_fp64(name):
+    cfg = {"tiny": synth.CONFIGS["tiny"],
+           "small_r5": synth.custom(2, 8, 6, 20, 20, 5, seed=3, dist="normal"),
+           "rect": synth.custom(3, 5, 7, 17, 29, 3, seed=4)}[name]
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    ref = torch.nn.functional.conv2d(I.double(), W.double()).numpy()
+    assert O.shape == ref.shape
+    np.testing.assert_allclose(O, ref, rtol=0, atol=1e-12 * max(1.0, np.abs(ref).max()))
+
+
+def test_linearity_exact():
+    I1 = _int_data((2, 3, 10, 9), 1)
+    I2 = _int_data((2, 3, 10, 9), 2)
+    W1 = _int_data((4, 3, 3, 3), 3)
+    W2 = _int_data((4, 3, 3, 3), 4)
+    a = np.float32(3.0)
+    np.testing.assert_array_equal(oracle.conv_fp64(a * I1 + I2, W1),
+                                  3.0 * oracle.conv_fp64(I1, W1) + oracle.conv_fp64(I2, W1))
+    np.testing.assert_array_equal(oracle.conv_fp64(I1, a * W1 + W2),
+                                  3.0 * oracle.conv_fp64(I1, W1) + oracle.conv_fp64(I1, W2))
+
+
+@pytest.mark.parametrize("r,p0,q0", [(3, 0, 0), (3, 1, 2), (5, 4, 1), (2, 1, 1)])
+def test_delta_kernel_shifts_input(r, p0, q0):
+    C = 4
+    I = np.random.default_rng(9).standard_normal((2, C, 12, 11)).astype(np.float32)
+    W = np.zeros((C, C, r, r), dtype=np.float32)
+    for c in range(C):
+        W[c, c, p0, q0] = 1.0
+    O = oracle.conv_fp64(I, W)
+    Ho, Wo = 12 - r + 1, 11 - r + 1
+    np.testing.assert_array_equal(O, I[:, :, p0:p0 + Ho, q0:q0 + Wo].astype(np.float64))
+
+
+def test_shift_equivariance():
+    I = _int_data((1, 3, 16, 16), 5)
+    W = _int_data((2, 3, 3, 3), 6)
+    dy, dx = 2, 3
+    Is = np.zeros_like(I)
+    Is[:, :, dy:, dx:] = I[:, :, :16 - dy, :16 - dx]
+    O = oracle.conv_fp64(I, W)
+    Os = oracle.conv_fp64(Is, W)
+    # output of shifted input, shifted back, equals the original on the overlap
+    np.testing.assert_array_equal(Os[:, :, dy:, dx:], O[:, :, :14 - dy, :14 - dx])
+
+
+def test_c_additivity_zero_batch_permutation():
+    I = _int_data((3, 6, 9, 9), 7)
+    W = _int_data((5, 6, 3, 3), 8)
+    O = oracle.conv_fp64(I, W)
+    np.testing.assert_array_equal(
+        O, oracle.conv_fp64(I[:, :2].copy(), W[:, :2].copy()) + oracle.conv_fp64(I[:, 2:].copy(), W[:, 2:].copy()))
+    np.testing.assert_array_equal(oracle.conv_fp64(I, np.zeros_like(W)), np.zeros_like(O))
+    for b in range(3):
+        np.testing.assert_array_equal(O[b:b + 1], oracle.conv_fp64(I[b:b + 1].copy(), W))
+    perm = np.array([3, 0, 4, 1, 2])
+    np.testing.assert_array_equal(oracle.conv_fp64(I, W[perm].copy()), O[:, perm])
+
+
+def test_rejects_bad_shapes():
+    with pytest.raises(ValueError):
+        oracle.conv_fp64(np.zeros((1, 1, 2, 2), np.float32), np.zeros((1, 1, 3, 3), np.float32))
+    with pytest.raises(TypeError):
+        oracle.conv_fp64(np.zeros((1, 1, 4, 4), np.float64), np.zeros((1, 1, 3, 3), np.float32))
+    cfg = synth.custom(1, 1, 1, 5, 5, 3)
+    I, W = synth.make_inputs(cfg)
+    with pytest.raises(ValueError):
+        oracle.conv_fp64_sampled(I, W, [[0, 0, 3, 0]])
