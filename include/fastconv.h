@@ -1,0 +1,156 @@
+/*
+ * fastconv.h -- C-ABI of the B200-native tiled fast-convolution forward pass.
+ *
+ * Problem statement (Eq. 5 "eq:forward"): one ConvNet
+ * layer's forward propagation
+ *
+ *     out[b][c'][i][j] = sum_{c<C} sum_{p<r} sum_{q<r} in[b][c][i+p][j+q] * w[c'][c][p][q]
+ *
+ * (valid cross-correlation, stride 1, no bias; readings R1-R3), for
+ * 0 <= i < H-r+1, 0 <= j < W-r+1, computed by one of
+ *
+ *   CONV_WINOGRAD     Winograd F(m^2, r^2)          (Eq. 1, Eq. 4)
+ *   CONV_REGULAR_FFT  Regular-FFT F(m^2, r^2)       (Eq. 2, "Regular-FFT")
+ *   CONV_GAUSS_FFT    Gauss-FFT G(m^2, r^2)         (Gauss' 3-mult product)
+ *   CONV_DIRECT       direct check path             (north_star step (4))
+ *
+ * in the paper's four stages: kernel transform (NK1), input
+ * transform over overlapping t = m+r-1 tiles (NK2), element-wise
+ * stage as E batched matrix products X_e = U_e V_e (NK3), and
+ * inverse transform + crop (NK4).  Every stage is a hand-written
+ * sm_100a CUDA kernel; the contraction runs on tcgen05 tensor cores with a
+ * 3xTF32 split (or an FFMA fallback).
+ *
+ * Conventions for every entry point:
+ *   - All tensors are fp32, contiguous, row-major: in [B][C][H][W],
+ *     w [Cout][C][r][r], out [B][Cout][H-r+1][W-r+1].
+ *   - Device pointers must be device memory of the plan's device, 16-byte
+ *     aligned (torch allocations are).  The caller owns in/w/out/workspace.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Functions never abort or throw; they return a conv_status.  On error a
+ *     thread-local detail string is available from conv_last_error().
+ *   - conv_forward is asynchronous on `stream` and performs no host sync.
+ *   - A plan is immutable after conv_plan/conv_plan_ex; concurrent forwards on
+ *     one plan are safe when their workspace and output buffers are distinct.
+ */
+#ifndef FASTCONV_H_
+#define FASTCONV_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CONV_OK = 0,
+    CONV_ERR_INVALID_ARG = 1,     /* bad sizes, NULL pointer, misaligned pointer, short workspace */
+    CONV_ERR_UNSUPPORTED = 2,     /* valid but not implemented (e.g. Winograd t > 8, FFT t > 64) */
+    CONV_ERR_OUT_OF_MEMORY = 3,   /* plan-constant allocation failed */
+    CONV_ERR_CUDA = 4,            /* a CUDA runtime/driver call or launch failed */
+    CONV_ERR_DEVICE_MISMATCH = 5  /* pointer or current device differs from the plan's device */
+} conv_status;
+
+typedef enum {
+    CONV_DIRECT = 0,
+    CONV_WINOGRAD = 1,
+    CONV_REGULAR_FFT = 2,
+    CONV_GAUSS_FFT = 3
+} conv_method;
+
+/* Contraction (NK3) implementation. */
+typedef enum {
+    CONV_GEMM_AUTO = 0,            /* tcgen05 3xTF32 */
+    CONV_GEMM_TCGEN05_3XTF32 = 1,  /* tcgen05.mma kind::tf32, TMEM accumulators, hi/lo split */
+    CONV_GEMM_FFMA = 2             /* fp32 FFMA tiled GEMM (the fallback it is measured against) */
+} conv_gemm_impl;
+
+typedef struct conv_plan_s *conv_plan_t;
+
+/* Geometry and algorithmic cost of a plan (PAPER.md
+ * Table "layer-stuff" P:1008-1042 with c = C, c' = C', alpha = 1). */
+typedef struct {
+    int B, C, Cout, H, W, r, m, method;
+    int Ho, Wo;
+    int t;              /* tile edge m + r - 1 */
+    int n_h, n_w;       /* tiles per dimension ceil((H-r+1)/m) */
+    int N;              /* tiles per image n_h * n_w */
+    int h;              /* stored columns per transformed row: t (Winograd) or t/2+1 (FFT) */
+    int E;              /* transformed elements per tile: t*t or t*h */
+    int planes;         /* real planes per element: 1 Winograd, 2 Regular (re/im), 3 Gauss */
+    long long BN;       /* B * N: rows of U_e / X_e */
+    long long BN_pad;   /* BN rounded up to 32 (row pitch of U and X) */
+    int gemm_Z, gemm_M, gemm_K;  /* batched contraction: Z products of [M x K] x [K x BN] */
+    size_t bytes_U, bytes_V, bytes_X;   /* workspace tensors (V includes the hi/lo split) */
+    size_t workspace_bytes;
+    /* algorithmic bytes / FLOPs per stage: [0]=NK1 kernel transform,
+     * [1]=NK2 input transform, [2]=NK3 contraction, [3]=NK4 output transform */
+    double alg_bytes[4];
+    double alg_flops[4];
+    double direct_flops;  /* 2 B C C' Ho Wo r^2 */
+} conv_plan_info;
+
+/* Host-only: validate arguments and fill `info` (no CUDA calls).  Errors:
+ * INVALID_ARG if any size < 1, H < r, W < r, or m < 1 for a fast method;
+ * UNSUPPORTED for Winograd with r < 2, m < 2 or t > 8, or FFT with t > 64. */
+conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r,
+                            conv_method method, int m, conv_plan_info *info);
+
+/* Create a plan on the current CUDA device (uploads ~KB of constants:
+ * Winograd matrices built exactly in rationals, DFT twiddles computed in fp64,
+ * both rounded once to fp32).  m is ignored for CONV_DIRECT.  `*out` is set
+ * only on CONV_OK; release with conv_destroy. */
+conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                      conv_method method, int m);
+conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                         conv_method method, int m, conv_gemm_impl gemm);
+
+conv_status conv_plan_get_info(conv_plan_t p, conv_plan_info *info);
+
+/* Bytes of device workspace conv_forward needs (U + V + X; 0 for CONV_DIRECT). */
+size_t conv_workspace_bytes(conv_plan_t p);
+
+/* Full forward pass, all four stages: NK1 w -> V, NK2 in -> U,
+ * NK3 (U, V) -> X, NK4 X -> out.  Asynchronous on `stream`. */
+conv_status conv_forward(conv_plan_t p, const float *in, const float *w, float *out,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
+/* Same, but synchronises and reports per-stage milliseconds measured with
+ * CUDA events: stage_ms[0..3] = NK1, NK2, NK3, NK4 (NK5 for CONV_DIRECT in [2]). */
+conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w, float *out,
+                                  void *workspace, size_t workspace_bytes, void *stream,
+                                  float stage_ms[4]);
+
+/* End-to-end call with HOST buffers: copies h_in, h_w (ideally pinned) to the
+ * caller-provided device buffers d_in, d_w, runs conv_forward, copies d_out
+ * back to h_out, all asynchronously on `stream` (the caller synchronises). */
+conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w, float *h_out,
+                              float *d_in, float *d_w, float *d_out,
+                              void *workspace, size_t workspace_bytes, void *stream);
+
+/* Run a single stage (0 = NK1, 1 = NK2, 2 = NK3, 3 = NK4) on the plan's
+ * workspace layout; used by stage-level tests.  Arguments a stage does not
+ * read may be NULL. */
+conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
+/* Byte offsets of V (hi), V_lo, U and X inside the workspace ([0..3]). */
+conv_status conv_workspace_layout(conv_plan_t p, size_t offsets[4]);
+
+/* The plan's Winograd matrices in fp64 (exact rationals): AT [m][t], BT [t][t],
+ * G [t][r], so that y = AT[(G g) . (BT d)] (Eq. 1).  UNSUPPORTED for
+ * non-Winograd plans. */
+conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, double *G);
+conv_status conv_winograd_matrices(int m, int r, double *AT, double *BT, double *G);
+
+void conv_destroy(conv_plan_t p);                 /* NULL-safe */
+const char *conv_status_string(conv_status s);    /* static string, never NULL */
+const char *conv_last_error(void);                /* thread-local detail of the last error */
+
+/* Kernel launches one conv_forward issues for this plan (for gpu_launches). */
+int conv_forward_launch_count(conv_plan_t p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTCONV_H_ */

@@ -1,0 +1,233 @@
+"""paper_1809_07851_b200 -- B200-native tiled fast-convolution forward pass.
+
+Thin ctypes binding over the C-ABI in ``include/fastconv.h`` (argument
+marshalling only: every stage runs in the hand-written sm_100a kernels of
+``libfastconv.so``).  PyTorch supplies device memory and the current stream.
+There is no CPU fallback: if the library is missing or a call fails, this
+module raises.
+
+Methods: ``"winograd"`` F(m^2, r^2) (Eq. 1/4),
+``"regular_fft"`` (Eq. 2), ``"gauss_fft"`` and the
+``"direct"`` check path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+from . import _build
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "fastconv.h")
+
+METHODS = {"direct": 0, "winograd": 1, "regular_fft": 2, "gauss_fft": 3}
+GEMMS = {"auto": 0, "tcgen05": 1, "ffma": 2}
+STATUS = {0: "CONV_OK", 1: "CONV_ERR_INVALID_ARG", 2: "CONV_ERR_UNSUPPORTED",
+          3: "CONV_ERR_OUT_OF_MEMORY", 4: "CONV_ERR_CUDA", 5: "CONV_ERR_DEVICE_MISMATCH"}
+
+
+class ConvError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        super().__init__("%s: %s" % (STATUS.get(status, status), detail))
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_int) for n in
+                 ("B", "C", "Cout", "H", "W", "r", "m", "method", "Ho", "Wo", "t", "n_h", "n_w",
+                  "N", "h", "E", "planes")] +
+                [("BN", ctypes.c_longlong), ("BN_pad", ctypes.c_longlong)] +
+                [(n, ctypes.c_int) for n in ("gemm_Z", "gemm_M", "gemm_K")] +
+                [(n, ctypes.c_size_t) for n in ("bytes_U", "bytes_V", "bytes_X", "workspace_bytes")] +
+                [("alg_bytes", ctypes.c_double * 4), ("alg_flops", ctypes.c_double * 4),
+                 ("direct_flops", ctypes.c_double)])
+
+    def as_dict(self) -> dict:
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if name.startswith("alg_") else v
+        return d
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = False):
+    """Load libfastconv.so (raise if absent: the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB):
+        if not build_if_missing:
+            raise RuntimeError("libfastconv.so is not built; run __graft_entry__.build() "
+                               "(or python paper_1809_07851_b200/_build.py)")
+        _build.build()
+    lib = ctypes.CDLL(_build.LIB)
+    vp, i, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    dp = ctypes.POINTER(ctypes.c_double)
+    fp = ctypes.POINTER(ctypes.c_float)
+    sigs = {
+        "conv_plan_query": ([i] * 8 + [ctypes.POINTER(PlanInfo)], i),
+        "conv_plan": ([ctypes.POINTER(vp)] + [i] * 8, i),
+        "conv_plan_ex": ([ctypes.POINTER(vp)] + [i] * 9, i),
+        "conv_plan_get_info": ([vp, ctypes.POINTER(PlanInfo)], i),
+        "conv_workspace_bytes": ([vp], sz),
+        "conv_forward": ([vp, vp, vp, vp, vp, sz, vp], i),
+        "conv_forward_profiled": ([vp, vp, vp, vp, vp, sz, vp, fp], i),
+        "conv_forward_host": ([vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i),
+        "conv_run_stage": ([vp, i, vp, vp, vp, vp, sz, vp], i),
+        "conv_workspace_layout": ([vp, ctypes.POINTER(sz)], i),
+        "conv_plan_winograd_matrices": ([vp, dp, dp, dp], i),
+        "conv_winograd_matrices": ([i, i, dp, dp, dp], i),
+        "conv_destroy": ([vp], None),
+        "conv_status_string": ([i], ctypes.c_char_p),
+        "conv_last_error": ([], ctypes.c_char_p),
+        "conv_forward_launch_count": ([vp], i),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def header_functions() -> list[str]:
+    """Names of every function include/fastconv.h declares."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(conv_[a-z_]+)\s*\(", src)))
+
+
+def _check(st: int):
+    if st != 0:
+        raise ConvError(st, load().conv_last_error().decode())
+
+
+def plan_query(B, C, Cout, H, W, r, method: str, m: int = 0) -> dict:
+    info = PlanInfo()
+    _check(load().conv_plan_query(B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def winograd_matrices(m: int, r: int):
+    """(AT [m][t], BT [t][t], G [t][r]) as nested lists of floats (exact rationals in fp64)."""
+    t = m + r - 1
+    AT = (ctypes.c_double * (m * t))()
+    BT = (ctypes.c_double * (t * t))()
+    G = (ctypes.c_double * (t * r))()
+    _check(load().conv_winograd_matrices(m, r, AT, BT, G))
+    return ([list(AT[i * t:(i + 1) * t]) for i in range(m)],
+            [list(BT[i * t:(i + 1) * t]) for i in range(t)],
+            [list(G[i * r:(i + 1) * r]) for i in range(t)])
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _check_tensor(x: torch.Tensor, name: str, shape=None):
+    if not isinstance(x, torch.Tensor):
+        raise TypeError("%s must be a torch.Tensor" % name)
+    if x.dtype != torch.float32:
+        raise TypeError("%s must be float32" % name)
+    if not x.is_cuda:
+        raise ValueError("%s must be a CUDA tensor" % name)
+    if not x.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+    if shape is not None and tuple(x.shape) != tuple(shape):
+        raise ValueError("%s has shape %s, expected %s" % (name, tuple(x.shape), tuple(shape)))
+
+
+class Plan:
+    """conv_plan(B, C, C', H, W, r, method, m) -- immutable; owns only host metadata + constants."""
+
+    def __init__(self, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto"):
+        lib = load()
+        h = ctypes.c_void_p()
+        _check(lib.conv_plan_ex(ctypes.byref(h), B, C, Cout, H, W, r, METHODS[method], m, GEMMS[gemm]))
+        self._h = h
+        self.method = method
+        info = PlanInfo()
+        _check(lib.conv_plan_get_info(h, ctypes.byref(info)))
+        self.info = info.as_dict()
+        self.workspace_bytes = int(lib.conv_workspace_bytes(h))
+        offs = (ctypes.c_size_t * 4)()
+        _check(lib.conv_workspace_layout(h, offs))
+        self.layout = {"V": offs[0], "Vlo": offs[1], "U": offs[2], "X": offs[3]}
+        self.launches = int(lib.conv_forward_launch_count(h))
+        self.in_shape = (B, C, H, W)
+        self.w_shape = (Cout, C, r, r)
+        self.out_shape = (B, Cout, H - r + 1, W - r + 1)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_destroy(h)
+            self._h = None
+
+    def alloc_workspace(self, device=None) -> torch.Tensor:
+        n = max(self.workspace_bytes, 16)
+        return torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+
+    def forward(self, x, w, out=None, workspace=None, stream=None) -> torch.Tensor:
+        _check_tensor(x, "input", self.in_shape)
+        _check_tensor(w, "weights", self.w_shape)
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.float32, device=x.device)
+        _check_tensor(out, "out", self.out_shape)
+        if workspace is None:
+            workspace = self.alloc_workspace(x.device)
+        _check(load().conv_forward(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                   workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                   _stream_ptr(stream)))
+        return out
+
+    def forward_profiled(self, x, w, out, workspace, stream=None):
+        ms = (ctypes.c_float * 4)()
+        _check(load().conv_forward_profiled(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                            workspace.data_ptr(), workspace.numel(), _stream_ptr(stream), ms))
+        return list(ms)
+
+    def forward_host(self, h_in, h_w, h_out, d_in, d_w, d_out, workspace, stream=None):
+        """End-to-end call with host (pinned) buffers; async on ``stream``."""
+        for t_, n in ((h_in, "h_in"), (h_w, "h_w"), (h_out, "h_out")):
+            if t_.is_cuda or not t_.is_contiguous() or t_.dtype != torch.float32:
+                raise ValueError("%s must be a contiguous float32 host tensor" % n)
+        _check(load().conv_forward_host(self._h, h_in.data_ptr(), h_w.data_ptr(), h_out.data_ptr(),
+                                        d_in.data_ptr(), d_w.data_ptr(), d_out.data_ptr(),
+                                        workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+
+    def run_stage(self, stage: int, x=None, w=None, out=None, workspace=None, stream=None):
+        p = lambda t_: 0 if t_ is None else t_.data_ptr()
+        _check(load().conv_run_stage(self._h, stage, p(x), p(w), p(out), workspace.data_ptr(),
+                                     workspace.numel(), _stream_ptr(stream)))
+
+    def winograd_matrices(self):
+        m, t, r = self.info["m"], self.info["t"], self.info["r"]
+        AT = (ctypes.c_double * (m * t))()
+        BT = (ctypes.c_double * (t * t))()
+        G = (ctypes.c_double * (t * r))()
+        _check(load().conv_plan_winograd_matrices(self._h, AT, BT, G))
+        return list(AT), list(BT), list(G)
+
+
+def forward(x: torch.Tensor, w: torch.Tensor, method: str = "winograd", m: int = 4,
+            gemm: str = "auto") -> torch.Tensor:
+    """One-shot forward: plans, allocates workspace/output with torch, runs on the current stream."""
+    B, C, H, W = x.shape
+    Cout, C2, r, _ = w.shape
+    if C2 != C:
+        raise ValueError("channel mismatch")
+    plan = Plan(B, C, Cout, H, W, r, method, m, gemm)
+    return plan.forward(x, w)

@@ -1,0 +1,605 @@
+// C-ABI of the fastconv library (include/fastconv.h): plan geometry, exact
+// Winograd matrices, DFT twiddles, workspace layout, and stage dispatch.
+//
+// Geometry follows PAPER.md P:956-965 (t = m + r - 1, N = ceil((x-r+1)/m)^2
+// per image, generalised to H != W), the half-spectrum width P:1062-1065
+// (t * ceil((t+1)/2) stored complex numbers = t * (t/2 + 1)), and the stage
+// costs of Table "layer-stuff" P:1008-1042.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "common.h"
+
+static thread_local char g_err[512] = "";
+
+void fc_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// ---------------------------------------------------------------------------
+// Exact rational Winograd matrices (PAPER.md P:274-290
+// "derived from Vandermonde matrices for Homogeneous Coordinate polynomials").
+// Points {0, 1, -1, 2, -2, 1/2, -1/2, ...} truncated to t-1 finite points plus
+// the point at infinity (reading R8).  With V the t x t evaluation
+// matrix of degree-<t polynomials (infinity row = leading coefficient), and
+// V_r, V_m its degree-<r / degree-<m analogues, correlation is the transpose
+// of polynomial multiplication:  y = V_m^T [ (V_r g) . (V^-T d) ], i.e.
+// A^T = V_m^T, G = V_r, B^T = V^-T; row i of B^T is scaled by the lcm of its
+// denominators and row i of G divided by it.
+// ---------------------------------------------------------------------------
+namespace {
+struct Frac {
+    long long n, d;
+};
+long long gcdll(long long a, long long b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        long long t = a % b;
+        a = b;
+        b = t;
+    }
+    return a ? a : 1;
+}
+Frac mk(long long n, long long d) {
+    if (d < 0) { n = -n; d = -d; }
+    long long g = gcdll(n, d);
+    return Frac{n / g, d / g};
+}
+Frac sub(Frac a, Frac b) { return mk(a.n * b.d - b.n * a.d, a.d * b.d); }
+Frac mul(Frac a, Frac b) { return mk(a.n * b.n, a.d * b.d); }
+Frac dvd(Frac a, Frac b) { return mk(a.n * b.d, a.d * b.n); }
+double val(Frac a) { return (double)a.n / (double)a.d; }
+}  // namespace
+
+conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G) {
+    const int t = m + r - 1;
+    if (m < 2 || r < 2 || t > 8) {
+        fc_set_error("Winograd F(%d,%d): need m>=2, r>=2, t=m+r-1<=8", m, r);
+        return CONV_ERR_UNSUPPORTED;
+    }
+    static const Frac pts[7] = {{0, 1}, {1, 1}, {-1, 1}, {2, 1}, {-2, 1}, {1, 2}, {-1, 2}};
+    Frac V[8][8], Inv[8][8];
+    for (int i = 0; i < t; ++i)
+        for (int j = 0; j < t; ++j) {
+            if (i < t - 1) {
+                Frac p = {1, 1};
+                for (int e = 0; e < j; ++e) p = mul(p, pts[i]);
+                V[i][j] = p;
+            } else {
+                V[i][j] = mk(j == t - 1 ? 1 : 0, 1);  // infinity: leading coefficient
+            }
+            Inv[i][j] = mk(i == j ? 1 : 0, 1);
+        }
+    // Gauss-Jordan inverse in exact rationals
+    for (int col = 0; col < t; ++col) {
+        int piv = col;
+        while (piv < t && V[piv][col].n == 0) ++piv;
+        if (piv == t) {
+            fc_set_error("singular Vandermonde matrix");
+            return CONV_ERR_UNSUPPORTED;
+        }
+        for (int j = 0; j < t; ++j) {
+            Frac x = V[col][j]; V[col][j] = V[piv][j]; V[piv][j] = x;
+            x = Inv[col][j]; Inv[col][j] = Inv[piv][j]; Inv[piv][j] = x;
+        }
+        Frac d = V[col][col];
+        for (int j = 0; j < t; ++j) {
+            V[col][j] = dvd(V[col][j], d);
+            Inv[col][j] = dvd(Inv[col][j], d);
+        }
+        for (int i = 0; i < t; ++i) {
+            if (i == col || V[i][col].n == 0) continue;
+            Frac f = V[i][col];
+            for (int j = 0; j < t; ++j) {
+                V[i][j] = sub(V[i][j], mul(f, V[col][j]));
+                Inv[i][j] = sub(Inv[i][j], mul(f, Inv[col][j]));
+            }
+        }
+    }
+    // B^T = (V^-1)^T : BT[i][j] = Inv[j][i]
+    Frac bt[8][8], gm[8][8];
+    for (int i = 0; i < t; ++i)
+        for (int j = 0; j < t; ++j) bt[i][j] = Inv[j][i];
+    // G = V_r (t x r), infinity row selects coefficient r-1
+    for (int i = 0; i < t; ++i)
+        for (int j = 0; j < r; ++j) {
+            if (i < t - 1) {
+                Frac p = {1, 1};
+                for (int e = 0; e < j; ++e) p = mul(p, pts[i]);
+                gm[i][j] = p;
+            } else {
+                gm[i][j] = mk(j == r - 1 ? 1 : 0, 1);
+            }
+        }
+    // row scaling: move denominators of B^T rows into G rows
+    for (int i = 0; i < t; ++i) {
+        long long L = 1;
+        for (int j = 0; j < t; ++j) L = L / gcdll(L, bt[i][j].d) * bt[i][j].d;
+        for (int j = 0; j < t; ++j) bt[i][j] = mul(bt[i][j], mk(L, 1));
+        for (int j = 0; j < r; ++j) gm[i][j] = dvd(gm[i][j], mk(L, 1));
+    }
+    // A^T = V_m^T (m x t)
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < t; ++j) {
+            Frac p;
+            if (j < t - 1) {
+                p = Frac{1, 1};
+                for (int e = 0; e < i; ++e) p = mul(p, pts[j]);
+            } else {
+                p = mk(i == m - 1 ? 1 : 0, 1);
+            }
+            AT[i * t + j] = val(p);
+        }
+    for (int i = 0; i < t; ++i) {
+        for (int j = 0; j < t; ++j) BT[i * t + j] = val(bt[i][j]);
+        for (int j = 0; j < r; ++j) G[i * r + j] = val(gm[i][j]);
+    }
+    return CONV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Geometry + algorithmic cost
+// ---------------------------------------------------------------------------
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
+                             Geometry *g, conv_plan_info *info, conv_gemm_impl gemm) {
+    if (B < 1 || C < 1 || Cout < 1 || H < 1 || W < 1 || r < 1) {
+        fc_set_error("sizes must be >= 1 (B=%d C=%d C'=%d H=%d W=%d r=%d)", B, C, Cout, H, W, r);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (H < r || W < r) {
+        fc_set_error("image %dx%d smaller than kernel %d", H, W, r);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (method < CONV_DIRECT || method > CONV_GAUSS_FFT) {
+        fc_set_error("unknown method %d", method);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (method != CONV_DIRECT && m < 1) {
+        fc_set_error("output tile m must be >= 1 (got %d)", m);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (gemm < CONV_GEMM_AUTO || gemm > CONV_GEMM_FFMA) {
+        fc_set_error("unknown gemm implementation %d", (int)gemm);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if ((long long)B * C * H * W >= (1LL << 40) || (long long)Cout * C * r * r >= (1LL << 40)) {
+        fc_set_error("tensor too large");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    Geometry G = {};
+    G.B = B; G.C = C; G.Cout = Cout; G.H = H; G.W = W; G.r = r; G.method = method;
+    G.Ho = H - r + 1;
+    G.Wo = W - r + 1;
+    if (method == CONV_DIRECT) {
+        G.m = 0;
+    } else {
+        G.m = m;
+        G.t = m + r - 1;
+        if (method == CONV_WINOGRAD) {
+            if (r < 2 || m < 2 || G.t > 8) {
+                fc_set_error("Winograd F(%d,%d) unsupported: need r>=2, m>=2, t<=8 (t=%d)", m, r, G.t);
+                return CONV_ERR_UNSUPPORTED;
+            }
+            G.h = G.t;
+            G.planes = 1;
+        } else {
+            if (G.t > FC_MAX_T) {
+                fc_set_error("FFT tile t=%d exceeds %d", G.t, FC_MAX_T);
+                return CONV_ERR_UNSUPPORTED;
+            }
+            G.h = G.t / 2 + 1;  // == ceil((t+1)/2)
+            G.planes = method == CONV_REGULAR_FFT ? 2 : 3;
+        }
+        G.n_h = (G.Ho + m - 1) / m;
+        G.n_w = (G.Wo + m - 1) / m;
+        G.N = G.n_h * G.n_w;
+        G.E = G.t * G.h;
+        G.BN = (long long)B * G.N;
+        G.BN_pad = (G.BN + 31) / 32 * 32;
+        if (method == CONV_REGULAR_FFT) {  // real embedding of the complex product
+            G.Z = G.E; G.M = 2 * Cout; G.K = 2 * C;
+        } else if (method == CONV_GAUSS_FFT) {
+            G.Z = 3 * G.E; G.M = Cout; G.K = C;
+        } else {
+            G.Z = G.E; G.M = Cout; G.K = C;
+        }
+        G.Kp = (G.K + 3) / 4 * 4;
+    }
+    *g = G;
+    if (info) {
+        conv_plan_info I;
+        memset(&I, 0, sizeof(I));
+        I.B = B; I.C = C; I.Cout = Cout; I.H = H; I.W = W; I.r = r; I.m = G.m; I.method = method;
+        I.Ho = G.Ho; I.Wo = G.Wo; I.t = G.t; I.n_h = G.n_h; I.n_w = G.n_w; I.N = G.N; I.h = G.h;
+        I.E = G.E; I.planes = G.planes; I.BN = G.BN; I.BN_pad = G.BN_pad;
+        I.gemm_Z = G.Z; I.gemm_M = G.M; I.gemm_K = G.K;
+        I.direct_flops = 2.0 * B * (double)C * Cout * G.Ho * G.Wo * r * r;
+        if (method != CONV_DIRECT) {
+            const int split = (gemm != CONV_GEMM_FFMA);
+            I.bytes_U = (size_t)G.Z * G.K * G.BN_pad * 4;
+            I.bytes_V = (size_t)G.Z * G.M * G.Kp * 4 * (split ? 2 : 1);
+            I.bytes_X = (size_t)G.Z * G.M * G.BN_pad * 4;
+            I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
+            // Table layer-stuff, c=C, c'=C', alpha=1; wE = reals per tile
+            const double wE = (double)G.planes * G.E * (method == CONV_WINOGRAD ? 1 : 1);
+            const double BCN = (double)B * C * G.N, BCpN = (double)B * Cout * G.N;
+            const double CCp = (double)C * Cout;
+            const double BN = (double)B * G.N;
+            const double wEr = method == CONV_GAUSS_FFT ? 3.0 * G.E : (method == CONV_REGULAR_FFT ? 2.0 * G.E : (double)G.E);
+            (void)wE;
+            I.alg_bytes[0] = 4.0 * CCp * r * r + 4.0 * wEr * CCp;
+            I.alg_bytes[1] = 4.0 * B * C * (double)H * W + 4.0 * wEr * BCN;
+            I.alg_bytes[2] = 4.0 * wEr * (BN * C + CCp + BN * Cout);
+            I.alg_bytes[3] = 4.0 * wEr * BCpN + 4.0 * B * Cout * (double)G.Ho * G.Wo;
+            // element-wise FLOPs: 2t^2 BNCC' / 8 t h BNCC' / 6 t h BNCC'
+            const double k = method == CONV_WINOGRAD ? 2.0 : (method == CONV_REGULAR_FFT ? 8.0 : 6.0);
+            I.alg_flops[2] = k * G.E * BN * CCp;
+        } else {
+            I.alg_bytes[2] = 4.0 * B * C * (double)H * W + 4.0 * Cout * C * r * r +
+                             4.0 * B * Cout * (double)G.Ho * G.Wo;
+            I.alg_flops[2] = I.direct_flops;
+        }
+        *info = I;
+    }
+    return CONV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *conv_status_string(conv_status s) {
+    switch (s) {
+        case CONV_OK: return "CONV_OK";
+        case CONV_ERR_INVALID_ARG: return "CONV_ERR_INVALID_ARG";
+        case CONV_ERR_UNSUPPORTED: return "CONV_ERR_UNSUPPORTED";
+        case CONV_ERR_OUT_OF_MEMORY: return "CONV_ERR_OUT_OF_MEMORY";
+        case CONV_ERR_CUDA: return "CONV_ERR_CUDA";
+        case CONV_ERR_DEVICE_MISMATCH: return "CONV_ERR_DEVICE_MISMATCH";
+    }
+    return "CONV_ERR_UNKNOWN";
+}
+
+const char *conv_last_error(void) { return g_err; }
+
+conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r, conv_method method, int m,
+                            conv_plan_info *info) {
+    Geometry g;
+    return fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &g, info, CONV_GEMM_AUTO);
+}
+
+conv_status conv_winograd_matrices(int m, int r, double *AT, double *BT, double *G) {
+    if (!AT || !BT || !G) {
+        fc_set_error("NULL output pointer");
+        return CONV_ERR_INVALID_ARG;
+    }
+    return fc_winograd_rational(m, r, AT, BT, G);
+}
+
+conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                         conv_method method, int m, conv_gemm_impl gemm) {
+    if (!out) {
+        fc_set_error("NULL plan pointer");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_plan_s *p = (conv_plan_s *)calloc(1, sizeof(conv_plan_s));
+    if (!p) return CONV_ERR_OUT_OF_MEMORY;
+    if (gemm == CONV_GEMM_AUTO) gemm = fc_tcgen05_available() ? CONV_GEMM_TCGEN05_3XTF32 : CONV_GEMM_FFMA;
+    if (gemm == CONV_GEMM_TCGEN05_3XTF32 && !fc_tcgen05_available()) {
+        free(p);
+        fc_set_error("tcgen05 contraction not available in this build");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    conv_status st = fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &p->g, &p->info, gemm);
+    if (st != CONV_OK) { free(p); return st; }
+    p->gemm = gemm;
+    const Geometry &g = p->g;
+    ConvConsts &cc = p->host_consts;
+    memset(&cc, 0, sizeof(cc));
+    if (method == CONV_WINOGRAD) {
+        st = fc_winograd_rational(g.m, g.r, p->AT64, p->BT64, p->G64);
+        if (st != CONV_OK) { free(p); return st; }
+        for (int i = 0; i < g.t * g.t; ++i) cc.BT[i] = (float)p->BT64[i];
+        for (int i = 0; i < g.t * g.r; ++i) cc.G[i] = (float)p->G64[i];
+        for (int i = 0; i < g.m * g.t; ++i) cc.AT[i] = (float)p->AT64[i];
+    } else if (method != CONV_DIRECT) {
+        for (int j = 0; j < g.t; ++j) {  // twiddles in fp64, rounded once (reading R11)
+            const double ang = 2.0 * M_PI * (double)j / (double)g.t;
+            cc.cosv[j] = (float)cos(ang);
+            cc.sinv[j] = (float)sin(ang);
+        }
+    }
+    cudaError_t e = cudaGetDevice(&p->device);
+    if (e != cudaSuccess) {
+        fc_set_error("cudaGetDevice: %s", cudaGetErrorString(e));
+        free(p);
+        return CONV_ERR_CUDA;
+    }
+    if (method != CONV_DIRECT) {
+        e = cudaMalloc(&p->d_consts, sizeof(ConvConsts));
+        if (e != cudaSuccess) {
+            fc_set_error("cudaMalloc(consts): %s", cudaGetErrorString(e));
+            free(p);
+            return e == cudaErrorMemoryAllocation ? CONV_ERR_OUT_OF_MEMORY : CONV_ERR_CUDA;
+        }
+        e = cudaMemcpy(p->d_consts, &cc, sizeof(ConvConsts), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            fc_set_error("cudaMemcpy(consts): %s", cudaGetErrorString(e));
+            cudaFree(p->d_consts);
+            free(p);
+            return CONV_ERR_CUDA;
+        }
+        p->off_V = 0;
+        const size_t vb = (size_t)g.Z * g.M * g.Kp * 4;
+        p->off_Vlo = align256(vb);
+        const size_t vtot = align256(p->info.bytes_V);
+        p->off_U = vtot;
+        p->off_X = vtot + align256(p->info.bytes_U);
+        p->ws_bytes = p->info.workspace_bytes;
+        if (gemm == CONV_GEMM_FFMA) p->off_Vlo = 0;
+    }
+    *out = p;
+    return CONV_OK;
+}
+
+conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                      conv_method method, int m) {
+    return conv_plan_ex(out, B, C, Cout, H, W, r, method, m, CONV_GEMM_AUTO);
+}
+
+void conv_destroy(conv_plan_t p) {
+    if (!p) return;
+    if (p->d_consts) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != p->device) cudaSetDevice(p->device);
+        cudaFree(p->d_consts);
+        if (cur >= 0 && cur != p->device) cudaSetDevice(cur);
+    }
+    free(p);
+}
+
+conv_status conv_plan_get_info(conv_plan_t p, conv_plan_info *info) {
+    if (!p || !info) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    *info = p->info;
+    return CONV_OK;
+}
+
+size_t conv_workspace_bytes(conv_plan_t p) { return p ? p->ws_bytes : 0; }
+
+conv_status conv_workspace_layout(conv_plan_t p, size_t offsets[4]) {
+    if (!p || !offsets) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    offsets[0] = p->off_V;
+    offsets[1] = p->off_Vlo;
+    offsets[2] = p->off_U;
+    offsets[3] = p->off_X;
+    return CONV_OK;
+}
+
+conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, double *G) {
+    if (!p || !AT || !BT || !G) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->g.method != CONV_WINOGRAD) {
+        fc_set_error("not a Winograd plan");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    memcpy(AT, p->AT64, sizeof(double) * p->g.m * p->g.t);
+    memcpy(BT, p->BT64, sizeof(double) * p->g.t * p->g.t);
+    memcpy(G, p->G64, sizeof(double) * p->g.t * p->g.r);
+    return CONV_OK;
+}
+
+int conv_forward_launch_count(conv_plan_t p) {
+    if (!p) return 0;
+    return p->g.method == CONV_DIRECT ? 1 : 4;
+}
+
+// -- pointer checks ----------------------------------------------------------
+static conv_status check_dev_ptr(const conv_plan_s *p, const void *ptr, const char *name) {
+    if (!ptr) {
+        fc_set_error("%s is NULL", name);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (((uintptr_t)ptr) & 15) {
+        fc_set_error("%s is not 16-byte aligned", name);
+        return CONV_ERR_INVALID_ARG;
+    }
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fc_set_error("%s: cudaPointerGetAttributes: %s", name, cudaGetErrorString(e));
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+        fc_set_error("%s is not device memory", name);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (a.device != p->device) {
+        fc_set_error("%s lives on device %d, plan on device %d", name, a.device, p->device);
+        return CONV_ERR_DEVICE_MISMATCH;
+    }
+    return CONV_OK;
+}
+
+static conv_status check_device(const conv_plan_s *p) {
+    int cur = -1;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess) {
+        fc_set_error("cudaGetDevice: %s", cudaGetErrorString(e));
+        return CONV_ERR_CUDA;
+    }
+    if (cur != p->device) {
+        fc_set_error("current device %d != plan device %d", cur, p->device);
+        return CONV_ERR_DEVICE_MISMATCH;
+    }
+    return CONV_OK;
+}
+
+static conv_status launch_result(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) {
+        fc_set_error("%s: %s", what, cudaGetErrorString(e));
+        return CONV_ERR_CUDA;
+    }
+    return CONV_OK;
+}
+
+static conv_status run_stage(conv_plan_s *p, int stage, const float *in, const float *w, float *out,
+                             char *ws, cudaStream_t s) {
+    const Geometry &g = p->g;
+    float *V = (float *)(ws + p->off_V);
+    float *Vlo = p->gemm == CONV_GEMM_FFMA ? nullptr : (float *)(ws + p->off_Vlo);
+    float *U = (float *)(ws + p->off_U);
+    float *X = (float *)(ws + p->off_X);
+    switch (stage) {
+        case 0:
+            return launch_result(fc_launch_kernel_transform(g, p->d_consts, w, V, Vlo, Vlo != nullptr, s),
+                                 "NK1 kernel transform");
+        case 1:
+            return launch_result(fc_launch_input_transform(g, p->d_consts, in, U, s), "NK2 input transform");
+        case 2:
+            if (p->gemm == CONV_GEMM_FFMA)
+                return launch_result(fc_launch_gemm_ffma(g, V, U, X, s), "NK3 FFMA contraction");
+            return launch_result(fc_launch_gemm_tcgen05(g, V, Vlo, U, X, s), "NK3 tcgen05 contraction");
+        case 3:
+            return launch_result(fc_launch_output_transform(g, p->d_consts, X, out, s), "NK4 output transform");
+    }
+    fc_set_error("bad stage %d", stage);
+    return CONV_ERR_INVALID_ARG;
+}
+
+static conv_status check_forward_args(conv_plan_s *p, const float *in, const float *w, float *out,
+                                      void *ws, size_t ws_bytes) {
+    if (!p) {
+        fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_status st = check_device(p);
+    if (st) return st;
+    if ((st = check_dev_ptr(p, in, "in"))) return st;
+    if ((st = check_dev_ptr(p, w, "weights"))) return st;
+    if ((st = check_dev_ptr(p, out, "out"))) return st;
+    if (p->g.method != CONV_DIRECT) {
+        if (ws_bytes < p->ws_bytes) {
+            fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+            return CONV_ERR_INVALID_ARG;
+        }
+        if ((st = check_dev_ptr(p, ws, "workspace"))) return st;
+    }
+    return CONV_OK;
+}
+
+conv_status conv_forward(conv_plan_t p, const float *in, const float *w, float *out, void *ws,
+                         size_t ws_bytes, void *stream) {
+    conv_status st = check_forward_args(p, in, w, out, ws, ws_bytes);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p->g.method == CONV_DIRECT) return launch_result(fc_launch_direct(p->g, in, w, out, s), "NK5 direct");
+    for (int k = 0; k < 4; ++k) {
+        st = run_stage(p, k, in, w, out, (char *)ws, s);
+        if (st) return st;
+    }
+    return CONV_OK;
+}
+
+conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,
+                           void *ws, size_t ws_bytes, void *stream) {
+    if (!p) {
+        fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->g.method == CONV_DIRECT) {
+        fc_set_error("direct plans have no stages");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    conv_status st = check_device(p);
+    if (st) return st;
+    if (ws_bytes < p->ws_bytes) {
+        fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if ((st = check_dev_ptr(p, ws, "workspace"))) return st;
+    if (stage == 0 && (st = check_dev_ptr(p, w, "weights"))) return st;
+    if (stage == 1 && (st = check_dev_ptr(p, in, "in"))) return st;
+    if (stage == 3 && (st = check_dev_ptr(p, out, "out"))) return st;
+    return run_stage(p, stage, in, w, out, (char *)ws, (cudaStream_t)stream);
+}
+
+conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w, float *out,
+                                  void *ws, size_t ws_bytes, void *stream, float stage_ms[4]) {
+    conv_status st = check_forward_args(p, in, w, out, ws, ws_bytes);
+    if (st) return st;
+    if (!stage_ms) {
+        fc_set_error("NULL stage_ms");
+        return CONV_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t ev[5];
+    for (int i = 0; i < 5; ++i) {
+        if (cudaEventCreate(&ev[i]) != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaEventDestroy(ev[j]);
+            return launch_result(cudaGetLastError(), "cudaEventCreate");
+        }
+    }
+    for (int k = 0; k < 4; ++k) stage_ms[k] = 0.f;
+    cudaEventRecord(ev[0], s);
+    if (p->g.method == CONV_DIRECT) {
+        st = launch_result(fc_launch_direct(p->g, in, w, out, s), "NK5 direct");
+        cudaEventRecord(ev[1], s);
+        cudaEventSynchronize(ev[1]);
+        if (!st) cudaEventElapsedTime(&stage_ms[2], ev[0], ev[1]);
+    } else {
+        for (int k = 0; k < 4 && !st; ++k) {
+            st = run_stage(p, k, in, w, out, (char *)ws, s);
+            cudaEventRecord(ev[k + 1], s);
+        }
+        cudaEventSynchronize(ev[4]);
+        if (!st)
+            for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&stage_ms[k], ev[k], ev[k + 1]);
+    }
+    cudaError_t e = cudaGetLastError();
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    if (!st && e != cudaSuccess) st = launch_result(e, "profiled forward");
+    return st;
+}
+
+conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w, float *h_out,
+                              float *d_in, float *d_w, float *d_out, void *ws, size_t ws_bytes,
+                              void *stream) {
+    if (!p || !h_in || !h_w || !h_out) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_status st = check_forward_args(p, d_in, d_w, d_out, ws, ws_bytes);
+    if (st) return st;
+    const Geometry &g = p->g;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nin = (size_t)g.B * g.C * g.H * g.W * 4, nw = (size_t)g.Cout * g.C * g.r * g.r * 4;
+    const size_t nout = (size_t)g.B * g.Cout * g.Ho * g.Wo * 4;
+    cudaError_t e = cudaMemcpyAsync(d_in, h_in, nin, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_w, h_w, nw, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return launch_result(e, "H2D copy");
+    st = conv_forward(p, d_in, d_w, d_out, ws, ws_bytes, stream);
+    if (st) return st;
+    return launch_result(cudaMemcpyAsync(h_out, d_out, nout, cudaMemcpyDeviceToHost, s), "D2H copy");
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal declarations shared by the fastconv CUDA translation units.
+// (Product path only; nothing here is shared with oracle/.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/fastconv.h"
+
+#define FC_MAX_T 64          // largest FFT tile edge supported (Winograd: 8)
+
+// Device-side constants of a plan (fp32, rounded once from fp64 / exact rationals).
+// Row transform "L" is applied along tile rows (index a, the H axis) and
+// "R" along columns (index b, the W axis); forward 2-D transform is
+//     Y[k][l] = sum_a sum_b L[k][a] d[a][b] R[l][b]
+// Winograd: L = R = B^T (Eq. 4, "B f B^T"), kernel: G, inverse: A^T.
+// FFT: L[k][a] = R[k][a] = exp(-2 pi i k a / t), stored as twiddles.
+struct ConvConsts {
+    float BT[8 * 8];     // Winograd B^T [t][t]
+    float G[8 * 8];      // Winograd G [t][r]
+    float AT[8 * 8];     // Winograd A^T [m][t]
+    float cosv[FC_MAX_T];  // cos(2 pi j / t), j < t   (fp64 -> fp32)
+    float sinv[FC_MAX_T];  // sin(2 pi j / t)
+};
+
+struct Geometry {
+    int B, C, Cout, H, W, r, m, method;
+    int Ho, Wo, t, n_h, n_w, N, h, E, planes;
+    long long BN, BN_pad;
+    int Z, M, K;  // contraction batch / rows (output channels side) / reduction
+    int Kp;       // row pitch of V (K rounded up to 4 floats = 16 B, for TMA)
+};
+
+struct conv_plan_s {
+    Geometry g;
+    conv_gemm_impl gemm;
+    int device;
+    ConvConsts host_consts;
+    double AT64[64], BT64[64], G64[64];  // exact Winograd matrices (fp64)
+    ConvConsts *d_consts;                 // device copy
+    size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
+    conv_plan_info info;
+};
+
+// ---- host helpers (plan.cu) ----
+conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
+                             Geometry *g, conv_plan_info *info, conv_gemm_impl gemm);
+conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G);
+void fc_set_error(const char *fmt, ...);
+
+// ---- kernel launchers (return cudaGetLastError()) ----
+cudaError_t fc_launch_kernel_transform(const Geometry &g, const ConvConsts *dc, const float *w,
+                                       float *V, float *Vlo, int split, cudaStream_t s);
+cudaError_t fc_launch_input_transform(const Geometry &g, const ConvConsts *dc, const float *in,
+                                      float *U, cudaStream_t s);
+cudaError_t fc_launch_output_transform(const Geometry &g, const ConvConsts *dc, const float *X,
+                                       float *out, cudaStream_t s);
+cudaError_t fc_launch_gemm_ffma(const Geometry &g, const float *V, const float *U, float *X,
+                                cudaStream_t s);
+cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo,
+                                   const float *U, float *X, cudaStream_t s);
+cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w, float *out,
+                             cudaStream_t s);
+int fc_tcgen05_available();

@@ -1,0 +1,157 @@
+"""CPU-only checks of the product's host side: the C-ABI library loads and exports
+every function include/fastconv.h declares; argument validation; plan geometry
+(PAPER.md P:956-965); algorithmic byte/FLOP counts (Table
+layer-stuff); the exact Winograd matrices (Eq. 1)."""
+import ctypes
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_1809_07851_b200 as fc
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1809_07851_b200 import _build
+    _build.build()
+    return fc.load()
+
+
+def test_exports_every_header_symbol(lib):
+    names = fc.header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    # the binding wires exactly these names
+    for n in ("conv_plan", "conv_forward", "conv_destroy", "conv_plan_query", "conv_workspace_bytes"):
+        assert n in names
+
+
+def test_status_strings(lib):
+    for k, v in fc.STATUS.items():
+        assert lib.conv_status_string(k).decode() == v
+    assert lib.conv_status_string(99).decode() == "CONV_ERR_UNKNOWN"
+    lib.conv_destroy(None)  # NULL-safe
+
+
+@pytest.mark.parametrize("args,status", [
+    ((0, 4, 4, 16, 16, 3, "winograd", 2), 1),
+    ((1, 4, 4, 2, 16, 3, "winograd", 2), 1),      # H < r
+    ((1, 4, 4, 16, 16, 3, "regular_fft", 0), 1),  # m < 1
+    ((1, 4, 4, 16, 16, 3, "winograd", 7), 2),     # t = 9 > 8
+    ((1, 4, 4, 16, 16, 1, "winograd", 4), 2),     # r < 2
+    ((1, 4, 4, 99, 99, 3, "regular_fft", 63), 2),  # t = 65 > 64
+])
+def test_plan_query_rejects(lib, args, status):
+    with pytest.raises(fc.ConvError) as ei:
+        fc.plan_query(*args)
+    assert ei.value.status == status
+
+
+def test_direct_ignores_m(lib):
+    info = fc.plan_query(2, 3, 4, 10, 10, 3, "direct", -5)
+    assert info["Ho"] == 8 and info["workspace_bytes"] == 0
+
+
+@pytest.mark.parametrize("x,r,m,t,N", [(58, 3, 4, 6, 196), (6, 3, 4, 6, 1), (7, 3, 4, 6, 4),
+                                       (58, 3, 14, 16, 16), (31, 5, 27, 31, 1), (16, 3, 7, 9, 4),
+                                       (226, 3, 25, 27, 81)])
+def test_geometry(lib, x, r, m, t, N):
+    # N = ceil((x-r+1)/m)^2; SPEC S:46-48 worked examples for the first three
+    for method in ("winograd", "regular_fft", "gauss_fft"):
+        if method == "winograd" and t > 8:
+            continue
+        info = fc.plan_query(2, 3, 5, x, x, r, method, m)
+        assert info["t"] == t and info["N"] == N
+        assert info["n_h"] * info["n_w"] == N
+        if method == "winograd":
+            assert info["E"] == t * t and info["planes"] == 1
+        else:
+            assert info["h"] == (t + 1 + 1) // 2 and info["E"] == t * ((t + 2) // 2)  # t*ceil((t+1)/2)
+            assert info["planes"] == (2 if method == "regular_fft" else 3)
+        assert info["BN"] == 2 * N and info["BN_pad"] % 32 == 0 and info["BN_pad"] >= info["BN"]
+
+
+def test_half_spectrum_size_t3(lib):
+    # P:1065 / SPEC S:363: t = 3 -> t * ceil((t+1)/2) = 6 stored complex numbers
+    info = fc.plan_query(1, 1, 1, 5, 5, 2, "regular_fft", 2)
+    assert info["t"] == 3 and info["E"] == 6
+
+
+def test_rectangular_geometry(lib):
+    info = fc.plan_query(1, 1, 1, 20, 33, 3, "winograd", 4)
+    assert (info["n_h"], info["n_w"]) == (5, 8)
+
+
+def test_algorithmic_costs_vgg32(lib):
+    B, C, Co, x, r = 64, 256, 256, 58, 3
+    w4 = fc.plan_query(B, C, Co, x, x, r, "winograd", 4)
+    t, N = 6, 196
+    assert w4["alg_bytes"][1] == pytest.approx(4 * B * C * x * x + 4 * B * C * N * t * t)
+    assert w4["alg_bytes"][0] == pytest.approx(4 * C * Co * (r * r + t * t))
+    assert w4["alg_bytes"][3] == pytest.approx(4 * B * Co * N * (t * t + 16))
+    assert w4["alg_flops"][2] == pytest.approx(2 * t * t * B * N * C * Co)
+    assert w4["direct_flops"] == pytest.approx(2 * B * C * Co * 56 * 56 * 9)
+    f14 = fc.plan_query(B, C, Co, x, x, r, "regular_fft", 14)
+    g14 = fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14)
+    th = 16 * 9
+    assert f14["alg_flops"][2] == pytest.approx(8 * th * B * 16 * C * Co)
+    assert g14["alg_flops"][2] == pytest.approx(6 * th * B * 16 * C * Co)
+    assert g14["alg_bytes"][1] - 4 * B * C * x * x == pytest.approx(1.5 * (f14["alg_bytes"][1] - 4 * B * C * x * x))
+
+
+def _frac(v):
+    return Fraction(v).limit_denominator(1 << 16)
+
+
+@pytest.mark.parametrize("m,r", [(2, 3), (4, 3), (6, 3), (2, 5), (3, 2), (2, 2), (4, 5), (3, 4)])
+def test_winograd_exact_identity(lib, m, r):
+    """A^T [(G g) . (B^T d)] equals the valid correlation exactly in rationals (Eq. 1),
+    and the 2-D nesting A^T[(G g G^T) . (B^T d B)]A (Eq. 4) likewise."""
+    AT, BT, G = fc.winograd_matrices(m, r)
+    t = m + r - 1
+    AT = [[_frac(v) for v in row] for row in AT]
+    BT = [[_frac(v) for v in row] for row in BT]
+    G = [[_frac(v) for v in row] for row in G]
+    rng = np.random.default_rng(m * 10 + r)
+    for _ in range(5):
+        d = [Fraction(int(v)) for v in rng.integers(-9, 10, t)]
+        g = [Fraction(int(v)) for v in rng.integers(-9, 10, r)]
+        Gg = [sum(G[i][j] * g[j] for j in range(r)) for i in range(t)]
+        Bd = [sum(BT[i][j] * d[j] for j in range(t)) for i in range(t)]
+        y = [sum(AT[i][k] * Gg[k] * Bd[k] for k in range(t)) for i in range(m)]
+        assert y == [sum(g[p] * d[i + p] for p in range(r)) for i in range(m)]
+    D = [[Fraction(int(v)) for v in row] for row in rng.integers(-5, 6, (t, t))]
+    K = [[Fraction(int(v)) for v in row] for row in rng.integers(-5, 6, (r, r))]
+    mm = lambda A, Bm: [[sum(A[i][k] * Bm[k][j] for k in range(len(Bm))) for j in range(len(Bm[0]))]
+                        for i in range(len(A))]
+    tr = lambda A: [list(c) for c in zip(*A)]
+    GK = mm(mm(G, K), tr(G))
+    BD = mm(mm(BT, D), tr(BT))
+    Y = mm(mm(AT, [[GK[i][j] * BD[i][j] for j in range(t)] for i in range(t)]), tr(AT))
+    ref = [[sum(K[p][q] * D[i + p][j + q] for p in range(r) for q in range(r)) for j in range(m)]
+           for i in range(m)]
+    assert Y == ref
+
+
+def test_winograd_f23_matches_lavin_form(lib):
+    # SPEC S:288 F(2,3) (Lavin form) -- equal up to the sign of the infinity row/column
+    AT, BT, G = fc.winograd_matrices(2, 3)
+    assert np.allclose(np.abs(BT), np.abs([[1, 0, -1, 0], [0, 1, 1, 0], [0, -1, 1, 0], [0, 1, 0, -1]]))
+    assert np.allclose(G, [[1, 0, 0], [.5, .5, .5], [.5, -.5, .5], [0, 0, 1]])
+    assert np.allclose(np.abs(AT), np.abs([[1, 1, 1, 0], [0, 1, -1, -1]]))
+
+
+def test_winograd_matrices_reject(lib):
+    with pytest.raises(fc.ConvError):
+        fc.winograd_matrices(7, 3)
+
+
+def test_plan_without_gpu_fails_cleanly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    st = lib.conv_plan_ex(ctypes.byref(h), 1, 4, 4, 16, 16, 3, 1, 2, 0)
+    assert st == 4 and not h.value  # CONV_ERR_CUDA, no plan returned

@@ -1,0 +1,237 @@
+"""Parity of the CUDA path (through the C-ABI) against the fp64 oracle.
+
+Error metric (BASELINE.json north_star; reading R10):
+    err = max |y_gpu - O| / max |O|     over the compared outputs.
+Bars: Regular/Gauss-FFT <= 1e-5; Winograd t <= 6 (F(2,3), F(4,3), F(2,5)) <= 1e-4;
+Winograd F(6,3) (t = 8, "6x6 output tiles", reading R9) <= 5e-4; direct <= 1e-5.
+
+* reduced configs (full oracle, every output): each BASELINE config with its
+  batch cut to 1-2 images (channels, image size, kernel and tiles kept, so the
+  contraction spans several K-steps and tiles, and partial tiles are ragged);
+* full BASELINE sizes, in the launch configuration bench.py times: 4096 random
+  sampled outputs + the corners of the first/last planes, oracle evaluated at
+  exactly those outputs;
+* edge cases: single output, C = 1, rectangular images, ragged tails, m > Ho,
+  zero weights.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+fc = None
+
+
+def setup_module(module):
+    global fc
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1809_07851_b200 as _fc
+    _fc.load()
+    fc = _fc
+
+
+def tol(method, m, r):
+    if method == "winograd":
+        return 5e-4 if m + r - 1 >= 8 else 1e-4
+    return 1e-5
+
+
+GEMMS = ["ffma", "tcgen05"]
+
+
+def _gemm_ok(gemm):
+    if gemm == "tcgen05":
+        try:
+            fc.Plan(1, 4, 4, 8, 8, 3, "winograd", 2, "tcgen05")
+        except fc.ConvError as e:
+            pytest.skip("tcgen05 path unavailable: %s" % e)
+
+
+def run_gpu(I, W, method, m, gemm="auto"):
+    x, w = I.cuda(), W.cuda()
+    B, C, H, Wd = x.shape
+    p = fc.Plan(B, C, W.shape[0], H, Wd, W.shape[2], method, m, gemm)
+    y = p.forward(x, w)
+    torch.cuda.synchronize()
+    return y.cpu().numpy().astype(np.float64)
+
+
+def rel_err(y, O):
+    return float(np.abs(y - O).max() / max(np.abs(O).max(), 1e-30))
+
+
+# ---------------------------------------------------------------- reduced ---
+REDUCED_B = {"tiny": 1, "vgg3_2": 2, "vgg1_2": 1, "k5": 2, "deep": 2}
+
+
+def _reduced_cases():
+    for name, cfg in synth.CONFIGS.items():
+        for (method, m) in cfg.runs + (("direct", 0),):
+            yield name, method, m
+
+
+_oracle_cache = {}
+
+
+def _reduced(name):
+    if name not in _oracle_cache:
+        cfg = synth.CONFIGS[name]
+        I, W = synth.make_inputs(cfg)
+        I = I[:REDUCED_B[name]].contiguous()
+        _oracle_cache[name] = (I, W, oracle.conv_fp64(I, W))
+    return _oracle_cache[name]
+
+
+@pytest.mark.parametrize("gemm", GEMMS)
+@pytest.mark.parametrize("name,method,m", list(_reduced_cases()))
+def test_reduced_full_oracle(name, method, m, gemm):
+    if method == "direct" and gemm != "ffma":
+        pytest.skip("direct path has no contraction variant")
+    _gemm_ok(gemm)
+    I, W, O = _reduced(name)
+    y = run_gpu(I, W, method, m, gemm)
+    err = rel_err(y, O)
+    bar = tol(method, m, W.shape[2])
+    print("%s %s m=%d %s err=%.3e (bar %.0e)" % (name, method, m, gemm, err, bar))
+    assert err <= bar
+
+
+# ------------------------------------------------------------- full size ---
+_full_cache = {}
+
+
+def _full(name):
+    if name not in _full_cache:
+        _full_cache.clear()
+        cfg = synth.CONFIGS[name]
+        I, W = synth.make_inputs(cfg)
+        idx = synth.sample_output_indices(cfg, 4096, seed=17)
+        _full_cache[name] = (cfg, I, W, idx, oracle.conv_fp64_sampled(I, W, idx))
+    return _full_cache[name]
+
+
+def _full_cases():
+    for name in ("vgg3_2", "vgg1_2", "k5", "deep"):
+        cfg = synth.CONFIGS[name]
+        for (method, m) in cfg.runs:
+            yield name, method, m
+
+
+@pytest.mark.parametrize("name,method,m", list(_full_cases()))
+def test_full_size_sampled(name, method, m):
+    cfg, I, W, idx, Os = _full(name)
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)  # bench.py's launch config
+    x, w = I.cuda(), W.cuda()
+    y = p.forward(x, w)
+    sel = torch.as_tensor(idx, device="cuda")
+    ys = y[sel[:, 0], sel[:, 1], sel[:, 2], sel[:, 3]].double().cpu().numpy()
+    assert torch.isfinite(y).all()
+    err = rel_err(ys, Os)
+    print("FULL %s %s m=%d err=%.3e" % (name, method, m, err))
+    assert err <= tol(method, m, cfg.r)
+
+
+# ----------------------------------------------------------------- edges ---
+EDGE = [
+    ("single_output", synth.custom(1, 3, 2, 3, 3, 3, seed=21)),
+    ("c1", synth.custom(2, 1, 3, 11, 9, 3, seed=22)),
+    ("rect_ragged", synth.custom(3, 6, 5, 19, 33, 3, seed=23)),
+    ("r5_ragged", synth.custom(2, 7, 9, 23, 17, 5, seed=24)),
+    ("r2", synth.custom(2, 5, 6, 12, 12, 2, seed=25)),
+    ("odd_channels", synth.custom(3, 13, 11, 20, 20, 3, seed=26)),
+    ("many_cout", synth.custom(1, 8, 300, 10, 10, 3, seed=27)),
+]
+EDGE_RUNS = [("winograd", 2), ("winograd", 4), ("winograd", 6), ("regular_fft", 2), ("regular_fft", 5),
+             ("regular_fft", 13), ("gauss_fft", 3), ("gauss_fft", 8), ("regular_fft", 40),
+             ("direct", 0)]
+
+
+@pytest.mark.parametrize("gemm", GEMMS)
+@pytest.mark.parametrize("ename,cfg", EDGE)
+def test_edge_cases(ename, cfg, gemm):
+    _gemm_ok(gemm)
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    for method, m in EDGE_RUNS:
+        if method == "winograd" and (m + cfg.r - 1 > 8 or cfg.r < 2):
+            continue
+        if method != "winograd" and m + cfg.r - 1 > 64:
+            continue
+        y = run_gpu(I, W, method, m, gemm)
+        err = rel_err(y, O)
+        assert err <= tol(method, m, cfg.r), (ename, method, m, err)
+
+
+@pytest.mark.parametrize("method,m", [("winograd", 4), ("regular_fft", 6), ("gauss_fft", 6), ("direct", 0)])
+def test_zero_weights_give_zero(method, m):
+    cfg = synth.CONFIGS["tiny"]
+    I, W = synth.make_inputs(cfg)
+    y = run_gpu(I, torch.zeros_like(W), method, m)
+    assert np.all(y == 0.0)
+
+
+def test_regular_vs_gauss_agree():
+    cfg = synth.custom(2, 32, 16, 30, 30, 3, seed=31, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    for m in (6, 14):
+        a = run_gpu(I, W, "regular_fft", m)
+        b = run_gpu(I, W, "gauss_fft", m)
+        assert rel_err(a, b) <= 2e-6
+
+
+def test_linearity_gpu():
+    cfg = synth.custom(2, 16, 8, 20, 20, 3, seed=32, dist="normal")
+    I1, W = synth.make_inputs(cfg)
+    I2, _ = synth.make_inputs(cfg, seed=33)
+    for method, m in (("winograd", 4), ("regular_fft", 8), ("gauss_fft", 8)):
+        y = run_gpu(I1 + I2, W, method, m)
+        y12 = run_gpu(I1, W, method, m) + run_gpu(I2, W, method, m)
+        assert rel_err(y, y12) <= 2e-5
+
+
+def test_abi_errors_on_gpu():
+    cfg = synth.CONFIGS["tiny"]
+    I, W = synth.make_inputs(cfg)
+    x, w = I.cuda(), W.cuda()
+    p = fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2)
+    ws = p.alloc_workspace()
+    out = torch.empty(p.out_shape, device="cuda")
+    lib = fc.load()
+    s = torch.cuda.current_stream().cuda_stream
+    # misaligned input pointer
+    st = lib.conv_forward(p._h, x.data_ptr() + 4, w.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), s)
+    assert st == 1
+    # host pointer
+    st = lib.conv_forward(p._h, I.data_ptr(), w.data_ptr(), out.data_ptr(), ws.data_ptr(), ws.numel(), s)
+    assert st == 1
+    # short workspace
+    st = lib.conv_forward(p._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), ws.data_ptr(), 16, s)
+    assert st == 1
+    # NULL output
+    st = lib.conv_forward(p._h, x.data_ptr(), w.data_ptr(), None, ws.data_ptr(), ws.numel(), s)
+    assert st == 1
+    with pytest.raises(ValueError):
+        p.forward(x[:, :2].contiguous(), w)
+    assert p.launches == 4
+
+
+def test_forward_host_and_profiled():
+    cfg = synth.CONFIGS["tiny"]
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    p = fc.Plan(1, 4, 4, 16, 16, 3, "gauss_fft", 6)
+    hi, hw = I.pin_memory(), W.pin_memory()
+    ho = torch.empty(p.out_shape).pin_memory()
+    di, dw = torch.empty_like(I, device="cuda"), torch.empty_like(W, device="cuda")
+    do = torch.empty(p.out_shape, device="cuda")
+    ws = p.alloc_workspace()
+    p.forward_host(hi, hw, ho, di, dw, do, ws)
+    torch.cuda.synchronize()
+    assert rel_err(ho.numpy().astype(np.float64), O) <= 1e-5
+    ms = p.forward_profiled(di, dw, do, ws)
+    assert len(ms) == 4 and all(v >= 0 for v in ms)
