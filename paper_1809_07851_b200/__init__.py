@@ -70,7 +70,7 @@ def load(build_if_missing: bool = False):
             raise RuntimeError("libfastconv.so is not built; run __graft_entry__.build() "
                                "(or python paper_1809_07851_b200/_build.py)")
         _build.build()
-    lib = ctypes.CDLL(_build.LIB)
+    lib = ctypes.CDLL(os.environ.get("FASTCONV_LIB", _build.LIB))
     vp, i, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     dp = ctypes.POINTER(ctypes.c_double)
     fp = ctypes.POINTER(ctypes.c_float)

@@ -226,7 +226,8 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         if (method != CONV_DIRECT) {
             const int split = (gemm != CONV_GEMM_FFMA);
             I.bytes_U = (size_t)G.Z * G.K * G.BN_pad * 4;
-            I.bytes_V = (size_t)G.Z * G.M * G.Kp * 4 * (split ? 2 : 1);
+            const size_t vb = (size_t)G.Z * G.M * G.Kp * 4;  // V_hi, then V_lo at the next 256 B boundary
+            I.bytes_V = split ? align256(vb) + vb : vb;
             I.bytes_X = (size_t)G.Z * G.M * G.BN_pad * 4;
             I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
             // Table layer-stuff, c=C, c'=C', alpha=1; wE = reals per tile

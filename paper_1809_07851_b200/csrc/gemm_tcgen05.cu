@@ -1,9 +1,417 @@
-// NK3 on tcgen05 (placeholder until the tensor-core kernel lands).
+// NK3 on the 5th-generation tensor cores: the element-wise stage as Z batched
+// real products (Eq. 8 "multiplication of a matrix U_e of
+// size BN x C with a matrix V_e of size C x C'")
+//
+//     X_z [M x BN] = V_z [M x K] . U_z [K x BN]        z < Z
+//
+// computed in fp32 semantics with a 3xTF32 split (reading R11):
+// a = a_hi + a_lo with a_hi = rna_tf32(a), a_lo = a - a_hi, and
+//     V.U ~= V_lo.U_hi + V_hi.U_lo + V_hi.U_hi      (fp32 TMEM accumulation).
+// V_hi / V_lo are pre-split by NK1 (V is small); the U tile is split in shared
+// memory by four "splitter" warps between the TMA load and the MMA, so U is
+// read from HBM exactly once per CTA tile and never stored twice.
+//
+// Kernel anatomy (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: V_hi, V_lo (K-major, 128B swizzle) and U
+//               (MN-major, 128B swizzle with 32B atoms -- the only MN-major
+//               swizzle tcgen05 accepts for 32-bit operands) into a smem ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
+//               M=128 x N=BLOCK_N x K=8, D in TMEM, double-buffered)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> global X
+//   warps 8-11  splitter: U -> (rna(U), U - rna(U)) in smem, fence.proxy.async
+// mbarriers: full (TMA tx), split (splitter done), empty (MMA commit),
+// tmem_full (MMA commit), tmem_empty (epilogue drained).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+
 #include "common.h"
 
-int fc_tcgen05_available() { return 0; }
+namespace {
 
-cudaError_t fc_launch_gemm_tcgen05(const Geometry &, const float *, const float *, const float *, float *,
-                                   cudaStream_t) {
-    return cudaErrorNotSupported;
+constexpr int BLOCK_M = 128;
+constexpr int BLOCK_K = 32;  // 32 fp32 = one 128-byte swizzle row
+constexpr int NUM_THREADS = 384;
+
+template <int BLOCK_N, int STAGES>
+struct TcCfg {
+    static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 4;
+    static constexpr int B_BYTES = BLOCK_N * BLOCK_K * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
+    static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;         // bytes TMA lands per stage
+    static constexpr int TMEM_COLS = 2 * BLOCK_N;                  // two accumulators
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// shared-memory matrix descriptor (tcgen05 "version 1"), 128-byte swizzle
+// layout 2 = SWIZZLE_128B (K-major operands), layout 1 = SWIZZLE_128B_BASE32B (MN-major
+// 32-bit operands: 32-byte chunks XOR-swizzled within 128-byte rows, 4-row atoms)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version for sm_100
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+
+#define TMEM_LD_32(taddr, v)                                                                                      \
+    asm volatile(                                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                            \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),  \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),             \
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),             \
+          "=r"(v[30]), "=r"(v[31])                                                                                \
+        : "r"(taddr))
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+struct TileCoord {
+    int z, m0, n0;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(int T, int n_m, int n_n, int BLOCK_N) {
+    TileCoord c;
+    const int mb = T % n_m;
+    const int rest = T / n_m;
+    c.m0 = mb * BLOCK_M;
+    c.n0 = (rest % n_n) * BLOCK_N;
+    c.z = rest / n_n;
+    return c;
+}
+
+template <int BLOCK_N, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    nk3_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+                     const __grid_constant__ CUtensorMap tmB, float *__restrict__ X, int M, int K, long long NP,
+                     int Z) {
+    using Cfg = TcCfg<BLOCK_N, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t bar0 = base + STAGES * Cfg::STAGE_BYTES;
+    // barrier layout: full[S] split[S] empty[S] tfull[2] tempty[2] | tmem slot
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto split_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + 2 + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + 8 * (3 * STAGES + 4));
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int n_m = (M + BLOCK_M - 1) / BLOCK_M;
+    const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
+    const int num_tiles = Z * n_m * n_n;
+    const int num_k = (K + BLOCK_K - 1) / BLOCK_K;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(split_bar(s), 128);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(Cfg::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
+                const TileCoord tc = decode_tile(T, n_m, n_n, BLOCK_N);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
+                    mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
+                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BLOCK_K, tc.m0, tc.z);
+                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BLOCK_K, tc.m0, tc.z);
+#pragma unroll
+                    for (int j = 0; j < BLOCK_N / 32; ++j)
+                        tma_load_3d(sB + j * 4096, &tmB, full_bar(stage), tc.n0 + 32 * j, kb * BLOCK_K, tc.z);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            // kind::tf32, D f32, A K-major, B MN-major, M = 128, N = BLOCK_N
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(BLOCK_M >> 4) << 24);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
+                mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(full_bar(stage), phase);
+                    mbar_wait(split_bar(stage), phase);
+                    tc_fence_after();
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
+                    const uint32_t sBlo = sB + Cfg::B_BYTES;
+#pragma unroll
+                    for (int s = 0; s < BLOCK_K / 8; ++s) {
+                        // A: K-major SW128, +32 B per K=8 step; B: MN-major SW128, +1024 B per 8 K-rows
+                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 1024, 2);
+                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 1024, 2);
+                        const uint64_t b_hi = make_desc(sB + 1024 * s, 4096, 512, 1);
+                        const uint64_t b_lo = make_desc(sBlo + 1024 * s, 4096, 512, 1);
+                        const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
+#ifdef FC_DEBUG
+                        if (blockIdx.x == 0 && kb == 0 && s == 0 && T == (int)blockIdx.x)
+                            printf("[mma] tmem=%x idesc=%x adesc=%llx bdesc=%llx sA=%x\n", d_tmem, idesc,
+                                   (unsigned long long)a_hi, (unsigned long long)b_hi, sA);
+#endif
+                        mma_tf32(d_tmem, a_lo, b_hi, idesc, first);
+                        mma_tf32(d_tmem, a_hi, b_lo, idesc, 1u);
+                        mma_tf32(d_tmem, a_hi, b_hi, idesc, 1u);
+                    }
+                    mma_commit(empty_bar(stage));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(tfull_bar(acc));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
+            const TileCoord tc = decode_tile(T, n_m, n_n, BLOCK_N);
+            mbar_wait(tfull_bar(acc), acc_phase);
+            tc_fence_after();
+            const int row = tc.m0 + q * 32 + lane;
+            float *xrow = X + ((size_t)tc.z * M + row) * NP + tc.n0;
+#pragma unroll 1
+            for (int c = 0; c < BLOCK_N / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
+                TMEM_LD_32(taddr, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef FC_DEBUG
+                if (lane < 2 && q == 0 && blockIdx.x == 0 && c == 0)
+                    printf("[epi] T=%d row=%d tmem=%x v=%g %g %g %g\n", T, row, taddr, __uint_as_float(v[0]),
+                           __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
+#endif
+                if (row < M && tc.n0 + c * 32 < NP) {
+                    float4 *dst = reinterpret_cast<float4 *>(xrow + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty_bar(acc));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 8) {
+        // ------------------------------------------------ hi/lo splitter for U
+        const int st = threadIdx.x - 256;  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
+            for (int kb = 0; kb < num_k; ++kb) {
+                mbar_wait(full_bar(stage), phase);
+#ifdef FC_DEBUG
+                if (st == 0 && blockIdx.x == 0 && kb == 0) {
+                    const float *f = reinterpret_cast<const float *>(gbase + stage * Cfg::STAGE_BYTES);
+                    printf("[split] T=%d A[0..3]=%g %g %g %g  Alo0=%g  B[0..3]=%g %g %g %g\n", T, f[0], f[1], f[2], f[3],
+                           f[Cfg::A_BYTES / 4], f[2 * Cfg::A_BYTES / 4], f[2 * Cfg::A_BYTES / 4 + 1],
+                           f[2 * Cfg::A_BYTES / 4 + 2], f[2 * Cfg::A_BYTES / 4 + 3]);
+                }
+#endif
+                float4 *bh = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
+                float4 *bl = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES +
+                                                        Cfg::B_BYTES);
+#pragma unroll
+                for (int j = 0; j < Cfg::B_BYTES / 16 / 128; ++j) {
+                    const float4 v = bh[st + 128 * j];
+                    float4 hi, lo;
+                    hi.x = tf32_rna(v.x); lo.x = v.x - hi.x;
+                    hi.y = tf32_rna(v.y); lo.y = v.y - hi.y;
+                    hi.z = tf32_rna(v.z); lo.z = v.z - hi.z;
+                    hi.w = tf32_rna(v.w); lo.w = v.w - hi.w;
+                    bh[st + 128 * j] = hi;
+                    bl[st + 128 * j] = lo;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(split_bar(stage));
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+bool encode_3d(CUtensorMap *map, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+               uint64_t s2_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {s1_bytes, s2_bytes};
+    cuuint32_t box[3] = {b0, b1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <int BLOCK_N, int STAGES>
+cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
+                   cudaStream_t s) {
+    using Cfg = TcCfg<BLOCK_N, STAGES>;
+    CUtensorMap mA, mAlo, mB;
+    const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
+    const uint64_t Kp = (uint64_t)g.Kp;
+    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return cudaErrorInvalidValue;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(nk3_gemm_tcgen05<BLOCK_N, STAGES>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long n_m = (g.M + BLOCK_M - 1) / BLOCK_M;
+    const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
+    const long long tiles = (long long)g.Z * n_m * n_n;
+    const int grid = (int)(tiles < g_num_sms ? tiles : g_num_sms);
+    nk3_gemm_tcgen05<BLOCK_N, STAGES><<<grid, NUM_THREADS, Cfg::SMEM_BYTES, s>>>(mA, mAlo, mB, X, g.M, g.K,
+                                                                              g.BN_pad, g.Z);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int fc_tcgen05_available() { return get_encode() != nullptr; }
+
+cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
+                                   cudaStream_t s) {
+    if (!Vlo) return cudaErrorInvalidValue;
+    return launch<128, 3>(g, Vhi, Vlo, U, X, s);
 }

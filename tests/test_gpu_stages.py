@@ -37,12 +37,14 @@ def _ws_view(ws, off, count):
     return ws[off:off + 4 * count].view(torch.float32)
 
 
+@pytest.mark.parametrize("shape", [(2, 4, 3, 16, 14, 3), (3, 72, 160, 21, 19, 3)])
+@pytest.mark.parametrize("gemm", ["ffma", "tcgen05"])
 @pytest.mark.parametrize("method,m", [("winograd", 2), ("winograd", 4), ("regular_fft", 6), ("gauss_fft", 6),
                                       ("regular_fft", 5)])
-def test_stages_tiny(fc, method, m):
-    cfg = synth.custom(2, 4, 3, 16, 14, 3, seed=41)
+def test_stages(fc, method, m, gemm, shape):
+    cfg = synth.custom(*shape, seed=41)
     I, W = synth.make_inputs(cfg)
-    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, "ffma")
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm)
     info = p.info
     t, h, E, N, BN, BNp = info["t"], info["h"], info["E"], info["N"], info["BN"], info["BN_pad"]
     Z, M, K = info["gemm_Z"], info["gemm_M"], info["gemm_K"]
@@ -54,6 +56,10 @@ def test_stages_tiny(fc, method, m):
     p.run_stage(1, x=x, workspace=ws)
     torch.cuda.synchronize()
     V = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
+    if gemm == "tcgen05":  # NK1 stores the 3xTF32 split: V = V_hi + V_lo, V_hi exactly TF32
+        Vhi = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].cpu()
+        assert torch.all((Vhi.view(torch.int32) & 0x1FFF) == 0)
+        V = V + _ws_view(ws, p.layout["Vlo"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
     U = _ws_view(ws, p.layout["U"], Z * K * BNp).reshape(Z, K, BNp)[:, :, :BN].double().cpu().numpy()
     In = I.double().numpy()
     Wn = W.double().numpy()
@@ -64,7 +70,7 @@ def test_stages_tiny(fc, method, m):
         AT = np.array(AT).reshape(m, t)
         BT = np.array(BT).reshape(t, t)
         G = np.array(G).reshape(t, cfg.r)
-        Uref = np.einsum("ka,bcnab,lb->klcbn", BT, tiles, BT).reshape(E, C, BN)
+        Uref = np.einsum("ka,xcnay,ly->klcxn", BT, tiles, BT).reshape(E, C, BN)
         Vref = np.einsum("kp,ocpq,lq->kloc", G, Wn, G).reshape(E, Co, C)
         np.testing.assert_allclose(U, Uref, atol=2e-5 * np.abs(Uref).max())
         np.testing.assert_allclose(V, Vref, atol=2e-6 * np.abs(Vref).max())
