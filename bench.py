@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 tiled fast-convolution forward pass (BASELINE.json metric:
+"ms/layer & effective TFLOP/s (direct-conv FLOPs) + roofline fraction, 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fastconv|reference]
+
+A *step* is one full pass of the hot path: NK1 kernel transform,
+NK2 input transform, NK3 contraction, NK4 output transform + crop, over one batch
+of the workload (the paper times the kernel transform as part of the layer,
+P:455-460; reading R13).  Workload: BASELINE.json configs[1], the
+VGG-3.2-shaped layer (B=64 per GPU, C=C'=256, 58x58, r=3).  The (method, m) is
+chosen per the paper's comparison rule (each method at its fastest m):
+every (method, m) the config lists is timed briefly, the fastest is the headline
+and all are reported under "sweep".
+
+Timing: inputs resident in HBM; W untimed warm-up steps; K steps bracketed by a
+barrier + cuda synchronize on both sides, timed with CUDA events on the launching
+stream, max over ranks.  Inputs (221 MB per GPU) exceed the 126 MB L2, so no
+explicit flush.  nvidia-smi samples SM clocks and throttle reasons during the run.
+N > 1: launched by torchrun, one rank per GPU, every rank processes its own
+B=64 batch (weak scaling, no collective on the data path).
+
+``--impl reference`` times the fp64 CPU oracle (oracle/, the only other place this
+script runs it) on bounded samples of the same workload: the paper has no GPU
+implementation to compare against.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "ms/layer & effective TFLOP/s (direct-conv FLOPs) + roofline fraction, 1/2/4/8 B200"
+UNIT = "TFLOP/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+TF32_OVER_BF16 = 0.5  # nominal dense ratio (1.1 vs 2.25 PFLOP/s, B200_PROFILING.md)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return d, "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+# ------------------------------------------------------------------ clocks ---
+class ClockSampler:
+    """nvidia-smi sampler running while the GPU works (B200_PROFILING.md clocks line)."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        inside = [p for (t, p) in self.samples if t0 <= t <= t1]
+        used = inside if inside else [p for (t, p) in self.samples if t >= t0 - 2.0]
+        if not used:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in used if num(p[1]) is not None]
+        mx = [num(p[2]) for p in used if num(p[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in used for i in range(4) if p[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(used), "samples_in_timed_region": len(inside),
+                "power_w_max": max((num(p[3]) or 0.0) for p in used)}
+
+
+# --------------------------------------------------------------- reference ---
+def run_reference(args, rank, world):
+    """The oracle as the reference arm: bounded samples of the workload on host cores."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    cfg = synth.CONFIGS[args.workload]
+    I, W = synth.make_inputs(cfg.with_batch(1))
+    # calibrate: one image x 2 output channels, then size a step to the budget
+    co = 2
+    t = time.perf_counter()
+    oracle.conv_fp64(I, W[:co].contiguous())
+    per_co = max((time.perf_counter() - t) / co, 1e-4)
+    budget = max(0.5, args.reference_budget_s / max(1, args.steps + args.warmup))
+    co = int(max(1, min(cfg.Cout, budget / per_co)))
+    Ws = W[:co].contiguous()
+    flops = 2.0 * cfg.C * co * cfg.Ho * cfg.Wo * cfg.r * cfg.r
+    for _ in range(args.warmup):
+        oracle.conv_fp64(I, Ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.conv_fp64(I, Ws)
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    value = flops / dt / 1e12
+    sample = "1 image x %d of %d output channels of %s per step (%.3g of the layer's direct FLOPs)" % (
+        co, cfg.Cout, cfg.name, flops / cfg.direct_flops)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "B": cfg.B, "C": cfg.C, "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W,
+                       "r": cfg.r, "impl": "fp64 CPU direct-convolution oracle (oracle/conv_oracle.c)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, seconds: float):
+    """Oracle (as it stands) on a bounded sample: the first n images x a slice of output channels."""
+    import oracle
+    import synth
+    I, W = synth.make_inputs(cfg)
+    oracle.conv_fp64(I[:1].contiguous(), W[:2].contiguous())  # warm the OpenMP pool
+    t = time.perf_counter()
+    oracle.conv_fp64(I[:1].contiguous(), W[:8].contiguous())
+    per_img_co = max((time.perf_counter() - t) / 8, 1e-5)
+    work = seconds / per_img_co  # image x output-channel units that fit the budget
+    co = int(max(1, min(cfg.Cout, work)))
+    nb = int(max(1, min(cfg.B, work / co)))
+    Is, Ws = I[:nb].contiguous(), W[:co].contiguous()
+    t = time.perf_counter()
+    oracle.conv_fp64(Is, Ws)
+    dt = time.perf_counter() - t
+    flops = 2.0 * nb * cfg.C * co * cfg.Ho * cfg.Wo * cfg.r * cfg.r
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": "%d of %d images x %d of %d output channels of %s (%.3g of the layer's direct FLOPs), %.1f s"
+                      % (nb, cfg.B, co, cfg.Cout, cfg.name, flops / cfg.direct_flops, dt)}
+
+
+# ------------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fastconv", choices=["fastconv", "reference"])
+    ap.add_argument("--workload", default="vgg3_2")
+    ap.add_argument("--method", default="auto", help="auto (sweep) or winograd|regular_fft|gauss_fft|direct")
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--gemm", default="auto", choices=["auto", "tcgen05", "ffma"])
+    ap.add_argument("--sweep-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-baseline-s", type=float, default=12.0)
+    ap.add_argument("--reference-budget-s", type=float, default=120.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_1809_07851_b200 import parallel
+    rank, world, local = parallel.env_rank_world()
+    if args.impl == "reference":
+        if world > 1:
+            parallel.init("gloo")
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import synth
+    import paper_1809_07851_b200 as fc
+    rank, world, local = parallel.init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    fc.load()
+    cfg = synth.CONFIGS[args.workload]
+    peaks, peaks_src = load_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    bf16_burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
+    tf32_peak = bf16_burst * TF32_OVER_BF16
+
+    # weak scaling: every rank owns a full B-image batch (independent seeded draw per rank)
+    I, W = synth.make_inputs(cfg, seed=cfg.seed + 1000 * rank)
+    x, w = I.to(dev), W.to(dev)
+    out = torch.empty((cfg.B, cfg.Cout, cfg.Ho, cfg.Wo), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def time_plan(plan, ws, steps):
+        for _ in range(2):
+            plan.forward(x, w, out, ws)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(steps):
+            plan.forward(x, w, out, ws)
+        e.record(stream)
+        e.synchronize()
+        return s.elapsed_time(e) / steps
+
+    # ---- sweep (the paper's rule: each method at its fastest m) -----------------
+    runs = list(cfg.runs) if args.method == "auto" else [(args.method, args.m)]
+    sweep = {}
+    for method, m in runs:
+        plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
+        ws = plan.alloc_workspace(dev)
+        ms = parallel.max_over_ranks(time_plan(plan, ws, args.sweep_steps), dev)
+        sweep["%s/m=%d" % (method, m)] = {"method": method, "m": m, "t": plan.info["t"], "ms": ms,
+                                         "tflops": cfg.direct_flops * world / (ms * 1e-3) / 1e12}
+        del ws, plan
+        torch.cuda.empty_cache()
+    best = min(sweep.values(), key=lambda d: d["ms"])
+    method, m = best["method"], best["m"]
+    plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
+    ws = plan.alloc_workspace(dev)
+    info = plan.info
+    nst = 4 if method != "direct" else 1
+
+    # ---- timed region -------------------------------------------------------------
+    clocks = ClockSampler(local)
+    for _ in range(args.warmup):
+        plan.forward(x, w, out, ws)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    parallel.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    start.record(stream)
+    for k in range(args.steps):
+        if nst == 1:
+            ev[k][0].record(stream)
+            plan.forward(x, w, out, ws)
+            ev[k][1].record(stream)
+        else:
+            ev[k][0].record(stream)
+            for s in range(4):  # the four stage kernels of conv_forward, one event between each
+                plan.run_stage(s, x, w, out, ws)
+                ev[k][s + 1].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    parallel.barrier()
+    t_wall1 = time.time()
+    total_ms = start.elapsed_time(end)
+    total_ms = parallel.max_over_ranks(total_ms, dev)
+    clk = clocks.summary(t_wall0, t_wall1)
+    clocks.stop()
+    ms_step = total_ms / args.steps
+    stage_ms = [statistics.mean(ev[k][s].elapsed_time(ev[k][s + 1]) for k in range(args.steps))
+                for s in range(nst)]
+    value = cfg.direct_flops * world / (ms_step * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel ------------------------------------------
+    names = ["NK1 kernel transform", "NK2 input transform", "NK3 contraction", "NK4 output transform"]
+    stages = []
+    for s in range(nst):
+        tsec = stage_ms[s] * 1e-3
+        if nst == 4 and s == 2:
+            flops = info["alg_flops"][2]
+            peak = tf32_peak / 3.0
+            ach = flops / tsec / 1e12
+            stages.append({"kernel": names[s], "ms": stage_ms[s], "bound": "tensor", "achieved": ach,
+                           "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                           "hbm_gbs": info["alg_bytes"][2] / tsec / 1e9})
+        elif nst == 4:
+            ach = info["alg_bytes"][s] / tsec / 1e9
+            stages.append({"kernel": names[s], "ms": stage_ms[s], "bound": "hbm", "achieved": ach,
+                           "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak})
+        else:
+            ach = cfg.direct_flops / tsec / 1e12
+            stages.append({"kernel": "NK5 direct", "ms": stage_ms[s], "bound": "alu", "achieved": ach,
+                           "peak": None, "unit": "TFLOP/s", "frac": None})
+    dom = max(stages, key=lambda d: d["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            traffic = tj.get("%s/%s/m=%d" % (cfg.name, method, m), {}).get(dom["kernel"])
+        except Exception:
+            traffic = None
+    roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
+                "peak_source": ("%s: %s" % (peaks_src,
+                                            "HBM copy GB/s" if dom["bound"] == "hbm" else
+                                            "bf16 burst x 0.5 (TF32/BF16 nominal) / 3 (3xTF32 split)"))}
+    # whole-layer roofline (paper Eq. running-time, stage sum)
+    t_roof = 0.0
+    if nst == 4:
+        for s in range(4):
+            tb = info["alg_bytes"][s] / (hbm_peak * 1e9)
+            tc = info["alg_flops"][s] / (tf32_peak / 3.0 * 1e12) if s == 2 else 0.0
+            t_roof += max(tb, tc)
+    layer_frac = (t_roof * 1e3) / ms_step if t_roof else None
+
+    # ---- end to end through the public API (host buffers, copies in the region) ---
+    e2e = None
+    if nst == 4 or True:
+        hi_, hw_ = I.pin_memory(), W.pin_memory()
+        ho_ = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
+        torch.cuda.synchronize()
+        parallel.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = parallel.max_over_ranks(s0.elapsed_time(s1) / args.e2e_steps, dev)
+        e2e = {"value": cfg.direct_flops * world / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": I.numel() * 4 + W.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
+               "api": "conv_forward_host (pinned host in/w/out, H2D + 4 stage kernels + D2H per step)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_baseline_s)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "B_per_gpu": cfg.B, "global_batch": cfg.B * world, "C": cfg.C,
+                       "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": method, "m": m,
+                       "t": info["t"], "gemm": args.gemm if args.gemm != "auto" else "tcgen05_3xtf32",
+                       "l2": "no flush: inputs %.0f MB/GPU > 126 MB L2" % (I.numel() * 4 / 1e6),
+                       "parallelism": "dp%d (batch-sharded ranks, no collective on the data path)" % world,
+                       "arith": "fp32 storage; contraction 3xTF32 on tcgen05 with fp32 TMEM accumulation"},
+            "roofline": roofline,
+            "layer_roofline_frac": layer_frac,
+            "stages": stages,
+            "sweep": sweep,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": plan.launches * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    parallel.barrier()
+
+
+if __name__ == "__main__":
+    main()
