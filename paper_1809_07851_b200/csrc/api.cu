@@ -320,6 +320,7 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
             cc.sinv[j] = (float)sin(ang);
         }
     }
+    p->generic_transforms = getenv("FASTCONV_GENERIC_TRANSFORMS") != nullptr;
     cudaError_t e = cudaGetDevice(&p->device);
     if (e != cudaSuccess) {
         fc_set_error("cudaGetDevice: %s", cudaGetErrorString(e));
@@ -327,6 +328,11 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
         return CONV_ERR_CUDA;
     }
     if (method != CONV_DIRECT) {
+        if (method != CONV_WINOGRAD && (e = fc_init_twiddles()) != cudaSuccess) {
+            fc_set_error("twiddle upload: %s", cudaGetErrorString(e));
+            free(p);
+            return CONV_ERR_CUDA;
+        }
         e = cudaMalloc(&p->d_consts, sizeof(ConvConsts));
         if (e != cudaSuccess) {
             fc_set_error("cudaMalloc(consts): %s", cudaGetErrorString(e));
@@ -474,14 +480,26 @@ static conv_status run_stage(conv_plan_s *p, int stage, const float *in, const f
         case 0:
             return launch_result(fc_launch_kernel_transform(g, p->d_consts, w, V, Vlo, Vlo != nullptr, s),
                                  "NK1 kernel transform");
-        case 1:
+        case 1: {
+            int handled = 0;
+            if (!p->generic_transforms) {
+                cudaError_t e = fc_launch_transform_fast(g, p->host_consts, in, U, 1, s, &handled);
+                if (handled) return launch_result(e, "NK2 input transform");
+            }
             return launch_result(fc_launch_input_transform(g, p->d_consts, in, U, s), "NK2 input transform");
+        }
         case 2:
             if (p->gemm == CONV_GEMM_FFMA)
                 return launch_result(fc_launch_gemm_ffma(g, V, U, X, s), "NK3 FFMA contraction");
             return launch_result(fc_launch_gemm_tcgen05(g, V, Vlo, U, X, s), "NK3 tcgen05 contraction");
-        case 3:
+        case 3: {
+            int handled = 0;
+            if (!p->generic_transforms) {
+                cudaError_t e = fc_launch_transform_fast(g, p->host_consts, X, out, 0, s, &handled);
+                if (handled) return launch_result(e, "NK4 output transform");
+            }
             return launch_result(fc_launch_output_transform(g, p->d_consts, X, out, s), "NK4 output transform");
+        }
     }
     fc_set_error("bad stage %d", stage);
     return CONV_ERR_INVALID_ARG;

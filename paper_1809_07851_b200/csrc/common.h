@@ -39,6 +39,7 @@ struct conv_plan_s {
     ConvConsts host_consts;
     double AT64[64], BT64[64], G64[64];  // exact Winograd matrices (fp64)
     ConvConsts *d_consts;                 // device copy
+    int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
     conv_plan_info info;
 };
@@ -63,3 +64,7 @@ cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const fl
 cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w, float *out,
                              cudaStream_t s);
 int fc_tcgen05_available();
+cudaError_t fc_init_twiddles();
+// compile-time-t transforms; *handled = 0 when t has no specialisation
+cudaError_t fc_launch_transform_fast(const Geometry &g, const ConvConsts &hc, const float *src, float *dst,
+                                     int forward, cudaStream_t s, int *handled);

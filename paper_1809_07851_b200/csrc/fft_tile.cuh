@@ -1,0 +1,116 @@
+// Register-resident complex FFTs of compile-time size N (mixed radix,
+// Cooley-Tukey decimation in time; prime factors by dense DFT) used by the
+// FFT tile transforms.  The paper's CPU codelets come from FFTW's genfft and
+// "support arbitrary sizes"; here every size is unrolled
+// at compile time instead, so all indices and twiddle addresses are constants.
+//
+// Twiddles W_N^k = exp(2 pi i k / N) live in __constant__ memory, computed on the
+// host in fp64 and rounded once to fp32 (reading R11); after unrolling
+// each FFMA reads its twiddle straight from the constant bank.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace fct {
+
+struct cf {
+    float x, y;
+};
+
+constexpr int kTwiddleCount = 64 * 65 / 2 + 64;  // sum_{N<=64} N, with slack
+__constant__ float2 c_tw[kTwiddleCount];         // (cos, sin)(2 pi k / N) at tw_base(N) + k
+
+__host__ __device__ constexpr int tw_base(int N) { return N * (N - 1) / 2; }
+
+// a * W_N^(DIR*j) with the trivial angles special-cased at compile time
+template <int N, int DIR>
+__device__ __forceinline__ cf twiddle_mul(cf a, int j) {
+    j %= N;
+    if (j == 0) return a;
+    if (2 * j == N) return cf{-a.x, -a.y};
+    if (4 * j == N) return DIR > 0 ? cf{-a.y, a.x} : cf{a.y, -a.x};        // * (+-i)
+    if (4 * j == 3 * N) return DIR > 0 ? cf{a.y, -a.x} : cf{-a.y, a.x};    // * (-+i)
+    const float2 w = c_tw[tw_base(N) + j];
+    const float s = DIR > 0 ? w.y : -w.y;
+    return cf{fmaf(a.x, w.x, -a.y * s), fmaf(a.x, s, a.y * w.x)};
+}
+
+__host__ __device__ constexpr int radix_of(int n) {
+    if (n % 4 == 0 && n > 4) return 4;
+    for (int p = 2; p * p <= n; ++p)
+        if (n % p == 0) return p;
+    return n;
+}
+
+// dense DFT for small / prime sizes: X[k] = sum_n x[n] W_N^(DIR n k)
+template <int N, int DIR>
+__device__ __forceinline__ void dft_small(cf *x) {
+    if constexpr (N == 1) {
+        return;
+    } else if constexpr (N == 2) {
+        const cf a = x[0], b = x[1];
+        x[0] = cf{a.x + b.x, a.y + b.y};
+        x[1] = cf{a.x - b.x, a.y - b.y};
+    } else if constexpr (N == 4) {
+        const cf a = x[0], b = x[1], c = x[2], d = x[3];
+        const cf s0{a.x + c.x, a.y + c.y}, s1{a.x - c.x, a.y - c.y};
+        const cf s2{b.x + d.x, b.y + d.y}, s3{b.x - d.x, b.y - d.y};
+        // s3 * (DIR i)
+        const cf r3 = DIR > 0 ? cf{-s3.y, s3.x} : cf{s3.y, -s3.x};
+        x[0] = cf{s0.x + s2.x, s0.y + s2.y};
+        x[2] = cf{s0.x - s2.x, s0.y - s2.y};
+        x[1] = cf{s1.x + r3.x, s1.y + r3.y};
+        x[3] = cf{s1.x - r3.x, s1.y - r3.y};
+    } else {
+        cf y[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            cf acc = x[0];
+#pragma unroll
+            for (int n = 1; n < N; ++n) {
+                const cf t = twiddle_mul<N, DIR>(x[n], n * k);
+                acc.x += t.x;
+                acc.y += t.y;
+            }
+            y[k] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) x[k] = y[k];
+    }
+}
+
+// in-place FFT, natural order in and out
+template <int N, int DIR>
+__device__ __forceinline__ void fft(cf *x) {
+    constexpr int P = radix_of(N);
+    if constexpr (P == N) {
+        dft_small<N, DIR>(x);
+    } else {
+        constexpr int Q = N / P;
+        cf s[P][Q];
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1)
+#pragma unroll
+            for (int n2 = 0; n2 < Q; ++n2) s[n1][n2] = x[P * n2 + n1];
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) fft<Q, DIR>(s[n1]);
+#pragma unroll
+        for (int n1 = 1; n1 < P; ++n1)
+#pragma unroll
+            for (int k1 = 1; k1 < Q; ++k1) s[n1][k1] = twiddle_mul<N, DIR>(s[n1][k1], n1 * k1);
+#pragma unroll
+        for (int k1 = 0; k1 < Q; ++k1) {
+            cf t[P];
+#pragma unroll
+            for (int n1 = 0; n1 < P; ++n1) t[n1] = s[n1][k1];
+            dft_small<P, DIR>(t);
+#pragma unroll
+            for (int k2 = 0; k2 < P; ++k2) x[k1 + Q * k2] = t[k2];
+        }
+    }
+}
+
+}  // namespace fct
+
+// host: upload the twiddle table to the current device once (thread-safe)
+cudaError_t fc_init_twiddles();

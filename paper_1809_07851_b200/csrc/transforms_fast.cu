@@ -1,0 +1,390 @@
+// Fast NK2 / NK4 tile transforms, specialised on the tile edge t at compile time.
+//
+//  * Winograd (t <= 8): one thread per (channel, tile), the t x t tile in
+//    registers, U = B^T d B and Y = A^T X A as unrolled dense products whose
+//    matrix entries sit in the kernel-parameter constant bank (Eq. 4).
+//  * FFT (Regular and Gauss): a CTA owns 32 consecutive tiles of one channel.
+//    Row pass: each thread packs two real tile rows into one complex FFT of
+//    length t and splits the half spectra (real-input trick); column pass: one
+//    complex FFT of length t per (half-spectrum column, tile) from shared memory
+//    (P:1062-1069 half spectrum; P:501-515 arbitrary sizes).  Inverse: pruned
+//    column IFFT (keep rows a < m), then two cropped rows per complex IFFT with
+//    the self-conjugate bins' imaginary parts dropped (readings R5-R7).
+//
+// Stores of U and loads of X run along the tile index n (lanes = consecutive
+// tiles), so every warp access to the big intermediates is a 128-byte line.
+#include <mutex>
+
+#include "common.h"
+#include "fft_tile.cuh"
+
+using fct::cf;
+
+namespace {
+
+struct WinoMats {
+    float BT[64];
+    float AT[64];
+};
+
+// ----------------------------------------------------------- Winograd NK2 ---
+template <int T>
+__global__ void __launch_bounds__(128) nk2_wino(Geometry g, WinoMats wm, const float *__restrict__ in,
+                                                float *__restrict__ U) {
+    const long long n = (long long)blockIdx.x * 128 + threadIdx.x;
+    const int c = blockIdx.y;
+    if (n >= g.BN) return;
+    const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
+    const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+    const int y0 = ti * g.m, x0 = tj * g.m;
+    const float *src = in + ((size_t)b * g.C + c) * g.H * g.W + (size_t)y0 * g.W + x0;
+    float d[T][T];
+    if (y0 + T <= g.H && x0 + T <= g.W) {
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int q = 0; q < T; ++q) d[a][q] = __ldg(src + a * g.W + q);
+    } else {
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int q = 0; q < T; ++q)
+                d[a][q] = (y0 + a < g.H && x0 + q < g.W) ? __ldg(src + a * g.W + q) : 0.f;
+    }
+    float z[T][T];  // z[a][l] = sum_q d[a][q] BT[l][q]
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < T; ++q) s = fmaf(wm.BT[l * T + q], d[a][q], s);
+            z[a][l] = s;
+        }
+    const size_t estride = (size_t)g.K * g.BN_pad;
+    float *dst = U + (size_t)c * g.BN_pad + n;
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float s = 0.f;
+#pragma unroll
+            for (int a = 0; a < T; ++a) s = fmaf(wm.BT[k * T + a], z[a][l], s);
+            __stcs(dst + (size_t)(k * T + l) * estride, s);
+        }
+}
+
+// ----------------------------------------------------------- Winograd NK4 ---
+template <int T>
+__global__ void __launch_bounds__(128) nk4_wino(Geometry g, WinoMats wm, const float *__restrict__ X,
+                                                float *__restrict__ out) {
+    const long long n = (long long)blockIdx.x * 128 + threadIdx.x;
+    const int co = blockIdx.y;
+    if (n >= g.BN) return;
+    const int m = g.m;
+    const size_t estride = (size_t)g.M * g.BN_pad;
+    const float *src = X + (size_t)co * g.BN_pad + n;
+    float x[T][T];
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int l = 0; l < T; ++l) x[k][l] = __ldcs(src + (size_t)(k * T + l) * estride);
+    float z[T][T];  // z[a][l] = sum_k AT[a][k] x[k][l], a < m
+#pragma unroll
+    for (int a = 0; a < T - 1; ++a) {
+        if (a >= m) break;
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < T; ++k) s = fmaf(wm.AT[a * T + k], x[k][l], s);
+            z[a][l] = s;
+        }
+    }
+    const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
+    const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+    const int y0 = ti * m, x0 = tj * m;
+    float *dst = out + ((size_t)b * g.Cout + co) * g.Ho * g.Wo + (size_t)y0 * g.Wo + x0;
+#pragma unroll
+    for (int a = 0; a < T - 1; ++a) {
+        if (a >= m) break;
+#pragma unroll
+        for (int q = 0; q < T - 1; ++q) {
+            if (q >= m) break;
+            float s = 0.f;
+#pragma unroll
+            for (int l = 0; l < T; ++l) s = fmaf(wm.AT[q * T + l], z[a][l], s);
+            if (y0 + a < g.Ho && x0 + q < g.Wo) dst[a * g.Wo + q] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- FFT NK2 ---
+constexpr int FTN = 32;  // tiles per CTA
+
+template <int T>
+struct FftCfg {
+    static constexpr int H = T / 2 + 1;
+    static constexpr int S2 = (T * H) % 2 ? T * H : T * H + 1;  // odd stride (float2 units)
+};
+
+template <int T>
+__global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U) {
+    constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
+    extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
+    const int c = blockIdx.y;
+    const long long n0 = (long long)blockIdx.x * FTN;
+    for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
+        const int nn = it % FTN, p = it / FTN;
+        const int a0 = 2 * p, a1 = 2 * p + 1;
+        const long long n = n0 + nn;
+        cf z[T];
+        if (n < g.BN) {
+            const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
+            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+            const int y0 = ti * g.m, x0 = tj * g.m;
+            const float *src = in + ((size_t)b * g.C + c) * g.H * g.W;
+            const bool r0 = y0 + a0 < g.H, r1 = (a1 < T) && (y0 + a1 < g.H);
+            const float *row0 = src + (size_t)(y0 + a0) * g.W + x0;
+            const float *row1 = row0 + g.W;
+            if (x0 + T <= g.W) {
+#pragma unroll
+                for (int q = 0; q < T; ++q) {
+                    z[q].x = r0 ? __ldg(row0 + q) : 0.f;
+                    z[q].y = r1 ? __ldg(row1 + q) : 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < T; ++q) {
+                    const bool cx = x0 + q < g.W;
+                    z[q].x = (r0 && cx) ? __ldg(row0 + q) : 0.f;
+                    z[q].y = (r1 && cx) ? __ldg(row1 + q) : 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < T; ++q) z[q] = cf{0.f, 0.f};
+        }
+        fct::fft<T, -1>(z);
+        // split the spectra of the two real rows: Xa = (Z[l] + conj Z[-l]) / 2, Xb = (Z[l] - conj Z[-l]) / 2i
+        float2 *dst = zs + nn * S + a0 * H;
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+            const cf p_ = z[l], q_ = z[(T - l) % T];
+            dst[l] = make_float2(0.5f * (p_.x + q_.x), 0.5f * (p_.y - q_.y));
+            if (a1 < T) dst[H + l] = make_float2(0.5f * (p_.y + q_.y), -0.5f * (p_.x - q_.x));
+        }
+    }
+    __syncthreads();
+    const size_t estride = (size_t)g.K * g.BN_pad;
+    for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
+        const int nn = it % FTN, l = it / FTN;
+        const long long n = n0 + nn;
+        cf z[T];
+#pragma unroll
+        for (int a = 0; a < T; ++a) {
+            const float2 v = zs[nn * S + a * H + l];
+            z[a] = cf{v.x, v.y};
+        }
+        fct::fft<T, -1>(z);
+        if (n >= g.BN) continue;
+        if (g.method == CONV_REGULAR_FFT) {
+            float *d0 = U + (size_t)c * g.BN_pad + n;
+            float *d1 = U + (size_t)(g.C + c) * g.BN_pad + n;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+                const size_t e = (size_t)(k * H + l) * estride;
+                __stcs(d0 + e, z[k].x);
+                __stcs(d1 + e, z[k].y);
+            }
+        } else {  // Gauss: (U_r + U_i, U_r, U_i) in planes 0, 1, 2
+            float *d0 = U + (size_t)c * g.BN_pad + n;
+            const size_t pl = (size_t)g.E * estride;
+#pragma unroll
+            for (int k = 0; k < T; ++k) {
+                const size_t e = (size_t)(k * H + l) * estride;
+                __stcs(d0 + e, z[k].x + z[k].y);
+                __stcs(d0 + pl + e, z[k].x);
+                __stcs(d0 + 2 * pl + e, z[k].y);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- FFT NK4 ---
+template <int T>
+__global__ void __launch_bounds__(256) nk4_fft(Geometry g, const float *__restrict__ X, float *__restrict__ out) {
+    constexpr int H = FftCfg<T>::H;
+    const int m = g.m;
+    const int S = (m * H) % 2 ? m * H : m * H + 1;
+    extern __shared__ float2 zs[];  // [FTN][S]: tile nn, output row a < m, bin l
+    const int co = blockIdx.y;
+    const long long n0 = (long long)blockIdx.x * FTN;
+    const size_t estride = (size_t)g.M * g.BN_pad;
+    for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
+        const int nn = it % FTN, l = it / FTN;
+        const long long n = n0 + nn;
+        cf z[T];
+        if (n < g.BN) {
+            const float *s0 = X + (size_t)co * g.BN_pad + n;
+            if (g.method == CONV_REGULAR_FFT) {
+                const float *s1 = X + (size_t)(g.Cout + co) * g.BN_pad + n;
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const size_t e = (size_t)(k * H + l) * estride;
+                    z[k] = cf{__ldcs(s0 + e), __ldcs(s1 + e)};
+                }
+            } else {  // Gauss: Re = T1 - T3, Im = T1 + T2
+                const size_t pl = (size_t)g.E * estride;
+#pragma unroll
+                for (int k = 0; k < T; ++k) {
+                    const size_t e = (size_t)(k * H + l) * estride;
+                    const float t1 = __ldcs(s0 + e), t2 = __ldcs(s0 + pl + e), t3 = __ldcs(s0 + 2 * pl + e);
+                    z[k] = cf{t1 - t3, t1 + t2};
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < T; ++k) z[k] = cf{0.f, 0.f};
+        }
+        fct::fft<T, +1>(z);  // inverse along the tile's H axis (unnormalised; 1/t^2 sits in V)
+        float2 *dst = zs + nn * S + l;
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+            if (a < m) dst[a * H] = make_float2(z[a].x, z[a].y);
+    }
+    __syncthreads();
+    const int RP = (m + 1) / 2;
+    for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
+        const int nn = it % FTN, p = it / FTN;
+        const int a0 = 2 * p, a1 = 2 * p + 1;
+        const long long n = n0 + nn;
+        if (n >= g.BN) continue;
+        const float2 *ra = zs + nn * S + a0 * H;
+        const float2 *rb = ra + H;
+        const bool has1 = a1 < m;
+        cf z[T];
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+            float2 A = ra[l];
+            float2 Bv = has1 ? rb[l] : make_float2(0.f, 0.f);
+            if (l == 0 || 2 * l == T) {  // self-conjugate bins: imaginary part dropped (reading R7)
+                A.y = 0.f;
+                Bv.y = 0.f;
+            }
+            z[l] = cf{A.x - Bv.y, A.y + Bv.x};                       // A + i B
+            if (l > 0 && 2 * l < T) z[T - l] = cf{A.x + Bv.y, Bv.x - A.y};  // conj(A) + i conj(B)
+        }
+        fct::fft<T, +1>(z);
+        const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
+        const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+        const int y0 = ti * m + a0, x0 = tj * m;
+        float *d0 = out + ((size_t)b * g.Cout + co) * g.Ho * g.Wo + (size_t)y0 * g.Wo + x0;
+        const bool w0 = y0 < g.Ho, w1 = has1 && (y0 + 1 < g.Ho);
+#pragma unroll
+        for (int q = 0; q < T; ++q) {
+            if (q < m && x0 + q < g.Wo) {
+                if (w0) d0[q] = z[q].x;
+                if (w1) d0[g.Wo + q] = z[q].y;
+            }
+        }
+    }
+}
+
+template <int T>
+cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
+    constexpr int H = FftCfg<T>::H;
+    const unsigned nblk = (unsigned)((g.BN + FTN - 1) / FTN);
+    if (forward) {
+        const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(nk2_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cfg = true;
+        }
+        nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst);
+    } else {
+        const int Sm = (g.m * H) % 2 ? g.m * H : g.m * H + 1;
+        const size_t smem = sizeof(float2) * FTN * Sm;
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(nk4_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(float2) * FTN * FftCfg<T>::S2));
+            cfg = true;
+        }
+        nk4_fft<T><<<dim3(nblk, g.Cout), 256, smem, s>>>(g, src, dst);
+    }
+    return cudaGetLastError();
+}
+
+template <int T>
+cudaError_t launch_wino(const Geometry &g, const WinoMats &wm, const float *src, float *dst, bool forward,
+                        cudaStream_t s) {
+    const unsigned nblk = (unsigned)((g.BN + 127) / 128);
+    if (forward)
+        nk2_wino<T><<<dim3(nblk, g.C), 128, 0, s>>>(g, wm, src, dst);
+    else
+        nk4_wino<T><<<dim3(nblk, g.Cout), 128, 0, s>>>(g, wm, src, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t dispatch(const Geometry &g, const ConvConsts &hc, const float *src, float *dst, bool forward,
+                     cudaStream_t s, bool *handled) {
+    *handled = true;
+    if (g.method == CONV_WINOGRAD) {
+        WinoMats wm;
+        for (int i = 0; i < 64; ++i) {
+            wm.BT[i] = hc.BT[i];
+            wm.AT[i] = hc.AT[i];
+        }
+        switch (g.t) {
+            case 4: return launch_wino<4>(g, wm, src, dst, forward, s);
+            case 5: return launch_wino<5>(g, wm, src, dst, forward, s);
+            case 6: return launch_wino<6>(g, wm, src, dst, forward, s);
+            case 7: return launch_wino<7>(g, wm, src, dst, forward, s);
+            case 8: return launch_wino<8>(g, wm, src, dst, forward, s);
+        }
+        *handled = false;
+        return cudaSuccess;
+    }
+    switch (g.t) {
+#define FC_FFT_CASE(TT) \
+    case TT: return launch_fft<TT>(g, src, dst, forward, s);
+        FC_FFT_CASE(4) FC_FFT_CASE(5) FC_FFT_CASE(6) FC_FFT_CASE(7) FC_FFT_CASE(8) FC_FFT_CASE(9)
+        FC_FFT_CASE(10) FC_FFT_CASE(12) FC_FFT_CASE(13) FC_FFT_CASE(14) FC_FFT_CASE(15) FC_FFT_CASE(16)
+        FC_FFT_CASE(18) FC_FFT_CASE(20) FC_FFT_CASE(21) FC_FFT_CASE(24) FC_FFT_CASE(25) FC_FFT_CASE(27)
+        FC_FFT_CASE(28) FC_FFT_CASE(30) FC_FFT_CASE(31) FC_FFT_CASE(32)
+#undef FC_FFT_CASE
+    }
+    *handled = false;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t fc_init_twiddles() {
+    static std::mutex mu;
+    static unsigned long long done_mask = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && (done_mask >> dev) & 1ull) return cudaSuccess;
+    static float2 tab[fct::kTwiddleCount];
+    for (int N = 1; N <= 64; ++N)
+        for (int k = 0; k < N; ++k) {
+            const double ang = 2.0 * M_PI * (double)k / (double)N;
+            tab[fct::tw_base(N) + k] = make_float2((float)cos(ang), (float)sin(ang));
+        }
+    e = cudaMemcpyToSymbol(fct::c_tw, tab, sizeof(tab));
+    if (e == cudaSuccess && dev < 64) done_mask |= 1ull << dev;
+    return e;
+}
+
+cudaError_t fc_launch_transform_fast(const Geometry &g, const ConvConsts &hc, const float *src, float *dst,
+                                     int forward, cudaStream_t s, int *handled) {
+    bool h = false;
+    cudaError_t e = dispatch(g, hc, src, dst, forward != 0, s, &h);
+    *handled = h ? 1 : 0;
+    return e;
+}
