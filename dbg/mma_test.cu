@@ -1,5 +1,6 @@
 // Numeric check of tcgen05 kind::tf32 with A K-major SW128 and B MN-major SW128_BASE32B.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -83,7 +84,9 @@ __global__ void k(const float *Ag, const float *Bg, float *out, int lbo, int sbo
 int main() {
     static float hA[M * K], hB[K * N], hD[M * N];
     for (int i = 0; i < M * K; ++i) hA[i] = (float)((i * 7) % 13 - 6);
-    for (int i = 0; i < K * N; ++i) hB[i] = (float)((i * 5) % 11 - 5);
+    const bool trunc_test = getenv("TRUNC") != nullptr;
+    if (trunc_test) { for (int i = 0; i < M * K; ++i) hA[i] = 1.0f + 3.0f / 4096.0f; }
+    for (int i = 0; i < K * N; ++i) hB[i] = trunc_test ? 1.0f : (float)((i * 5) % 11 - 5);
     float *dA, *dB, *dD;
     cudaMalloc(&dA, sizeof(hA));
     cudaMalloc(&dB, sizeof(hB));

@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -314,18 +315,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                            f[2 * Cfg::A_BYTES / 4 + 2], f[2 * Cfg::A_BYTES / 4 + 3]);
                 }
 #endif
-                float4 *bh = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
+                const float4 *bh =
+                    reinterpret_cast<const float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
                 float4 *bl = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES +
                                                         Cfg::B_BYTES);
+                // the MMA reads U truncated to TF32 (measured: low 13 mantissa bits ignored), so the
+                // hi part is U itself and lo = U - trunc_tf32(U), exact in fp32
 #pragma unroll
                 for (int j = 0; j < Cfg::B_BYTES / 16 / 128; ++j) {
                     const float4 v = bh[st + 128 * j];
-                    float4 hi, lo;
-                    hi.x = tf32_rna(v.x); lo.x = v.x - hi.x;
-                    hi.y = tf32_rna(v.y); lo.y = v.y - hi.y;
-                    hi.z = tf32_rna(v.z); lo.z = v.z - hi.z;
-                    hi.w = tf32_rna(v.w); lo.w = v.w - hi.w;
-                    bh[st + 128 * j] = hi;
+                    float4 lo;
+                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                     bl[st + 128 * j] = lo;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -343,6 +346,268 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+    }
+}
+
+// ===========================================================================
+// cta_group::2 variant: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile
+// with M = 256 tcgen05.mma instructions issued by the leader CTA.  Rank r holds
+// rows [128 r, 128 r + 128) of the V tile (A operand) and columns
+// [r BLOCK_N/2, (r+1) BLOCK_N/2) of the U tile (B operand); each CTA's TMEM
+// receives its 128 rows x BLOCK_N columns.  Per SM this halves the bytes each
+// MMA cycle needs from shared memory and L2 (U is read once for C' <= 256).
+// Cross-CTA signalling: splitters arrive on the leader's split barrier, MMA
+// commits multicast to both CTAs' empty / tmem_full barriers, epilogues arrive
+// on the leader's tmem_empty barrier.
+// ===========================================================================
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_mc(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+template <int BLOCK_N, int STAGES>
+struct Tc2Cfg {
+    static constexpr int NH = BLOCK_N / 2;  // columns of U per CTA
+    static constexpr int A_BYTES = 128 * BLOCK_K * 4;
+    static constexpr int B_BYTES = NH * BLOCK_K * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BLOCK_N;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BLOCK_N, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    nk3_gemm_tcgen05_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+                         const __grid_constant__ CUtensorMap tmB, float *__restrict__ X, int M, int K, long long NP,
+                         int Z) {
+    using Cfg = Tc2Cfg<BLOCK_N, STAGES>;
+    static_assert(Cfg::TMEM_COLS <= 512, "TMEM holds 512 columns");
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t bar0 = base + STAGES * Cfg::STAGE_BYTES;
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto split_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + 2 + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + 8 * (3 * STAGES + 4));
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int n_m = (M + 255) / 256;
+    const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
+    const int num_tiles = Z * n_m * n_n;
+    const int num_k = (K + BLOCK_K - 1) / BLOCK_K;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(split_bar(s), 256);  // 128 splitter threads from each CTA (leader's copy is used)
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 256);  // both CTAs' epilogue threads (leader's copy is used)
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(Cfg::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto decode = [&](int T, int &z, int &m0, int &n0) {
+        const int mb = T % n_m, rest = T / n_m;
+        m0 = mb * 256;
+        n0 = (rest % n_n) * BLOCK_N;
+        z = rest / n_n;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (both CTAs load their halves)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int T = pair; T < num_tiles; T += npairs) {
+                int z, m0, n0;
+                decode(T, z, m0, n0);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
+                    mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
+                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BLOCK_K, m0 + 128 * (int)rank, z);
+                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BLOCK_K, m0 + 128 * (int)rank, z);
+#pragma unroll
+                    for (int j = 0; j < Cfg::NH / 32; ++j)
+                        tma_load_3d(sB + j * 4096, &tmB, full_bar(stage), n0 + (int)rank * Cfg::NH + 32 * j,
+                                    kb * BLOCK_K, z);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA only)
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int T = pair; T < num_tiles; T += npairs) {
+                mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait_cluster(split_bar(stage), phase);
+                    tc_fence_after();
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
+                    const uint32_t sBlo = sB + Cfg::B_BYTES;
+#pragma unroll
+                    for (int s = 0; s < BLOCK_K / 8; ++s) {
+                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 1024, 2);
+                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 1024, 2);
+                        const uint64_t b_hi = make_desc(sB + 1024 * s, 4096, 512, 1);
+                        const uint64_t b_lo = make_desc(sBlo + 1024 * s, 4096, 512, 1);
+                        const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
+                        mma_tf32_2sm(d_tmem, a_lo, b_hi, idesc, first);
+                        mma_tf32_2sm(d_tmem, a_hi, b_lo, idesc, 1u);
+                        mma_tf32_2sm(d_tmem, a_hi, b_hi, idesc, 1u);
+                    }
+                    mma_commit_2sm_mc(empty_bar(stage));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_2sm_mc(tfull_bar(acc));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {  // ---- epilogue (each CTA drains its 128 TMEM lanes)
+        const int q = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int T = pair; T < num_tiles; T += npairs) {
+            int z, m0, n0;
+            decode(T, z, m0, n0);
+            mbar_wait(tfull_bar(acc), acc_phase);
+            tc_fence_after();
+            const int row = m0 + 128 * (int)rank + q * 32 + lane;
+            float *xrow = X + ((size_t)z * M + row) * NP + n0;
+#pragma unroll 1
+            for (int c = 0; c < BLOCK_N / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
+                TMEM_LD_32(taddr, v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (row < M && n0 + c * 32 < NP) {
+                    float4 *dst = reinterpret_cast<float4 *>(xrow + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive_cluster(map_to_rank(tempty_bar(acc), 0));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 8) {  // ---- splitter: lo = U - tf32_trunc(U) (the MMA truncates U to its hi part)
+        const int st = threadIdx.x - 256;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int T = pair; T < num_tiles; T += npairs) {
+            for (int kb = 0; kb < num_k; ++kb) {
+                mbar_wait(full_bar(stage), phase);
+                const float4 *bh = reinterpret_cast<const float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
+                float4 *bl = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES +
+                                                        Cfg::B_BYTES);
+#pragma unroll
+                for (int j = 0; j < Cfg::B_BYTES / 16 / 128; ++j) {
+                    const float4 v = bh[st + 128 * j];
+                    float4 lo;
+                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    bl[st + 128 * j] = lo;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_cluster(map_to_rank(split_bar(stage), 0));
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
     }
 }
 
@@ -406,6 +671,52 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     return cudaGetLastError();
 }
 
+template <int BLOCK_N, int STAGES>
+cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
+                       cudaStream_t s) {
+    using Cfg = Tc2Cfg<BLOCK_N, STAGES>;
+    CUtensorMap mA, mAlo, mB;
+    const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
+    const uint64_t Kp = (uint64_t)g.Kp;
+    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return cudaErrorInvalidValue;
+    auto kern = nk3_gemm_tcgen05_2sm<BLOCK_N, STAGES>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long n_m = (g.M + 255) / 256;
+    const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
+    const long long tiles = (long long)g.Z * n_m * n_n;
+    const long long pairs = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int M_ = g.M, K_ = g.K, Z_ = g.Z;
+    long long NP_ = g.BN_pad;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, X, M_, K_, NP_, Z_);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int fc_tcgen05_available() { return get_encode() != nullptr; }
@@ -413,5 +724,7 @@ int fc_tcgen05_available() { return get_encode() != nullptr; }
 cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                                    cudaStream_t s) {
     if (!Vlo) return cudaErrorInvalidValue;
+    static const int force_1sm = getenv("FASTCONV_TC_1SM") != nullptr;
+    if (g.M > 128 && !force_1sm) return launch_2sm<256, 3>(g, Vhi, Vlo, U, X, s);
     return launch<128, 3>(g, Vhi, Vlo, U, X, s);
 }
