@@ -370,17 +370,10 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
     return r;
 }
+// Remote arrive with the default (.release.cta) semantics, as CUTLASS's ClusterBarrier
+// does: an explicit .release.cluster here costs a GPU-scope MEMBAR per arrival.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAITC_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAITC_%=;\n}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -443,12 +436,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(split_bar(s), 256);  // 128 splitter threads from each CTA (leader's copy is used)
+            mbar_init(split_bar(s), 8);  // one arrival per splitter warp, 4 warps x 2 CTAs (leader's copy)
             mbar_init(empty_bar(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 256);  // both CTAs' epilogue threads (leader's copy is used)
+            mbar_init(tempty_bar(a), 8);  // one arrival per epilogue warp, both CTAs (leader's copy)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -507,11 +500,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int T = pair; T < num_tiles; T += npairs) {
-                mbar_wait_cluster(tempty_bar(acc), acc_phase ^ 1);
+                mbar_wait(tempty_bar(acc), acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
                 for (int kb = 0; kb < num_k; ++kb) {
-                    mbar_wait_cluster(split_bar(stage), phase);
+                    mbar_wait(split_bar(stage), phase);
                     tc_fence_after();
                     const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
                     const uint32_t sAlo = sA + Cfg::A_BYTES;
@@ -567,7 +560,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive_cluster(map_to_rank(tempty_bar(acc), 0));
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(map_to_rank(tempty_bar(acc), 0));
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -594,7 +588,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     bl[st + 128 * j] = lo;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive_cluster(map_to_rank(split_bar(stage), 0));
+                __syncwarp();
+                if ((st & 31) == 0) mbar_arrive_cluster(map_to_rank(split_bar(stage), 0));
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
