@@ -234,8 +234,11 @@ def main():
         plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
         ws = plan.alloc_workspace(dev)
         ms = parallel.max_over_ranks(time_plan(plan, ws, args.sweep_steps), dev)
+        prof = [plan.forward_profiled(x, w, out, ws) for _ in range(3)]
+        stage_ms_sweep = [round(min(p[s] for p in prof), 4) for s in range(4)]
         sweep["%s/m=%d" % (method, m)] = {"method": method, "m": m, "t": plan.info["t"], "ms": ms,
-                                         "tflops": cfg.direct_flops * world / (ms * 1e-3) / 1e12}
+                                         "tflops": cfg.direct_flops * world / (ms * 1e-3) / 1e12,
+                                         "stage_ms": stage_ms_sweep}
         del ws, plan
         torch.cuda.empty_cache()
     best = min(sweep.values(), key=lambda d: d["ms"])
