@@ -395,35 +395,39 @@ __device__ __forceinline__ void mma_commit_2sm_mc(uint32_t bar) {
         : "memory");
 }
 
-template <int BLOCK_N, int STAGES>
+template <int BLOCK_N, int STAGES, int BK>
 struct Tc2Cfg {
     static constexpr int NH = BLOCK_N / 2;  // columns of U per CTA
-    static constexpr int A_BYTES = 128 * BLOCK_K * 4;
-    static constexpr int B_BYTES = NH * BLOCK_K * 4;
+    static constexpr int A_BYTES = 128 * BK * 4;
+    static constexpr int B_BYTES = NH * BK * 4;
     static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
     static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BLOCK_N;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 128 B)
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
-template <int BLOCK_N, int STAGES>
+template <int BLOCK_N, int STAGES, int BK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     nk3_gemm_tcgen05_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
-                         const __grid_constant__ CUtensorMap tmB, float *__restrict__ X, int M, int K, long long NP,
-                         int Z) {
-    using Cfg = Tc2Cfg<BLOCK_N, STAGES>;
+                         const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
+                         int M, int K, long long NP, int Z, int dbg) {
+    using Cfg = Tc2Cfg<BLOCK_N, STAGES, BK>;
+    static_assert(BK == 16 || BK == 32, "BK is one 64 B or 128 B swizzle row");
     static_assert(Cfg::TMEM_COLS <= 512, "TMEM holds 512 columns");
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t *gbase = smem_raw + (base - raw);
-    const uint32_t bar0 = base + STAGES * Cfg::STAGE_BYTES;
+    const uint32_t epi0 = base + STAGES * Cfg::STAGE_BYTES;  // epilogue staging (1024-aligned)
+    const uint32_t bar0 = epi0 + Cfg::EPI_BYTES;
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto split_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto empty_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + 2 + a); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + 8 * (3 * STAGES + 4));
+    uint32_t *tmem_slot =
+        reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES + 8 * (3 * STAGES + 4));
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int n_m = (M + 255) / 256;
     const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
     const int num_tiles = Z * n_m * n_n;
-    const int num_k = (K + BLOCK_K - 1) / BLOCK_K;
+    const int num_k = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -478,12 +483,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t sAlo = sA + Cfg::A_BYTES;
                     const uint32_t sB = sA + 2 * Cfg::A_BYTES;
                     mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
-                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BLOCK_K, m0 + 128 * (int)rank, z);
-                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BLOCK_K, m0 + 128 * (int)rank, z);
+                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BK, m0 + 128 * (int)rank, z);
+                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BK, m0 + 128 * (int)rank, z);
 #pragma unroll
                     for (int j = 0; j < Cfg::NH / 32; ++j)
-                        tma_load_3d(sB + j * 4096, &tmB, full_bar(stage), n0 + (int)rank * Cfg::NH + 32 * j,
-                                    kb * BLOCK_K, z);
+                        tma_load_3d(sB + j * (BK * 128), &tmB, full_bar(stage), n0 + (int)rank * Cfg::NH + 32 * j,
+                                    kb * BK, z);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -511,14 +516,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t sB = sA + 2 * Cfg::A_BYTES;
                     const uint32_t sBlo = sB + Cfg::B_BYTES;
 #pragma unroll
-                    for (int s = 0; s < BLOCK_K / 8; ++s) {
-                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 1024, 2);
-                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 1024, 2);
-                        const uint64_t b_hi = make_desc(sB + 1024 * s, 4096, 512, 1);
-                        const uint64_t b_lo = make_desc(sBlo + 1024 * s, 4096, 512, 1);
+                    for (int s = 0; s < BK / 8; ++s) {
+                        // A: K-major, 128B (BK=32) or 64B (BK=16) swizzle, 8-row atoms; +32 B per K=8.
+                        // B: MN-major 128B/32B-atom swizzle, n-blocks of BK rows x 128 B, 4-row atoms.
+                        constexpr uint32_t a_sbo = BK * 4 * 8, a_layout = BK == 32 ? 2u : 4u;
+                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, a_sbo, a_layout);
+                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, a_sbo, a_layout);
+                        const uint64_t b_hi = make_desc(sB + 1024 * s, BK * 128, 512, 1);
+                        const uint64_t b_lo = make_desc(sBlo + 1024 * s, BK * 128, 512, 1);
                         const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
-                        mma_tf32_2sm(d_tmem, a_lo, b_hi, idesc, first);
-                        mma_tf32_2sm(d_tmem, a_hi, b_lo, idesc, 1u);
+                        if (!(dbg & 2)) { mma_tf32_2sm(d_tmem, a_lo, b_hi, idesc, first);
+                        mma_tf32_2sm(d_tmem, a_hi, b_lo, idesc, 1u); }
                         mma_tf32_2sm(d_tmem, a_hi, b_hi, idesc, 1u);
                     }
                     mma_commit_2sm_mc(empty_bar(stage));
@@ -534,30 +542,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= 4 && warp < 8) {  // ---- epilogue (each CTA drains its 128 TMEM lanes)
+    } else if (warp >= 4 && warp < 8) {
+        // ---- epilogue: each warp drains its 32 TMEM lanes, 32 columns at a time, into a
+        // 128B-swizzled 32 x 32 smem tile and TMA-stores it (full-line, clipped at M / NP).
         const int q = warp & 3;
-        int acc = 0;
+        const uint32_t stage0 = epi0 + q * (2 * 4096);
+        int acc = 0, buf = 0;
         uint32_t acc_phase = 0;
         for (int T = pair; T < num_tiles; T += npairs) {
             int z, m0, n0;
             decode(T, z, m0, n0);
             mbar_wait(tfull_bar(acc), acc_phase);
             tc_fence_after();
-            const int row = m0 + 128 * (int)rank + q * 32 + lane;
-            float *xrow = X + ((size_t)z * M + row) * NP + n0;
+            const int row0 = m0 + 128 * (int)rank + q * 32;
 #pragma unroll 1
             for (int c = 0; c < BLOCK_N / 32; ++c) {
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
                 TMEM_LD_32(taddr, v);
+                // the staging buffer we are about to overwrite must have been read by its TMA store
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (row < M && n0 + c * 32 < NP) {
-                    float4 *dst = reinterpret_cast<float4 *>(xrow + c * 32);
+                const uint32_t sb = stage0 + buf * 4096;
+                const uint32_t rowaddr = sb + lane * 128;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                for (int j = 0; j < 8; ++j)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + ((j ^ (lane & 7)) << 4)),
+                                 "r"(v[4 * j]), "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                                 : "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0 && !(dbg & 4)) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                            &tmX),
+                        "r"(sb), "r"(n0 + 32 * c), "r"(row0), "r"(z)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
+                buf ^= 1;
             }
             tc_fence_before();
             __syncwarp();
@@ -598,6 +622,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
 
+    if (warp >= 4 && warp < 8 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     cluster_sync_all();
     if (warp == 1) {
@@ -666,18 +691,20 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     return cudaGetLastError();
 }
 
-template <int BLOCK_N, int STAGES>
+template <int BLOCK_N, int STAGES, int BK>
 cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                        cudaStream_t s) {
-    using Cfg = Tc2Cfg<BLOCK_N, STAGES>;
-    CUtensorMap mA, mAlo, mB;
+    using Cfg = Tc2Cfg<BLOCK_N, STAGES, BK>;
+    CUtensorMap mA, mAlo, mB, mX;
     const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
     const uint64_t Kp = (uint64_t)g.Kp;
-    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    const CUtensorMapSwizzle aswz = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BK, 128, aswz) ||
+        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BK, 128, aswz) ||
+        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+        !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
-    auto kern = nk3_gemm_tcgen05_2sm<BLOCK_N, STAGES>;
+    auto kern = nk3_gemm_tcgen05_2sm<BLOCK_N, STAGES, BK>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -707,7 +734,8 @@ cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, co
     cfg.numAttrs = 1;
     int M_ = g.M, K_ = g.K, Z_ = g.Z;
     long long NP_ = g.BN_pad;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, X, M_, K_, NP_, Z_);
+    static const int dbg = getenv("FASTCONV_TC_DBG") ? atoi(getenv("FASTCONV_TC_DBG")) : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_, dbg);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -720,6 +748,8 @@ cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const fl
                                    cudaStream_t s) {
     if (!Vlo) return cudaErrorInvalidValue;
     static const int force_1sm = getenv("FASTCONV_TC_1SM") != nullptr;
-    if (g.M > 128 && !force_1sm) return launch_2sm<256, 3>(g, Vhi, Vlo, U, X, s);
+    static const int bk32 = getenv("FASTCONV_TC_BK32") != nullptr;
+    if (g.M > 128 && !force_1sm)
+        return bk32 ? launch_2sm<256, 2, 32>(g, Vhi, Vlo, U, X, s) : launch_2sm<256, 6, 16>(g, Vhi, Vlo, U, X, s);
     return launch<128, 3>(g, Vhi, Vlo, U, X, s);
 }
