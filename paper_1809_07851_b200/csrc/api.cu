@@ -477,9 +477,16 @@ static conv_status run_stage(conv_plan_s *p, int stage, const float *in, const f
     float *U = (float *)(ws + p->off_U);
     float *X = (float *)(ws + p->off_X);
     switch (stage) {
-        case 0:
+        case 0: {
+            int handled = 0;
+            if (!p->generic_transforms) {
+                cudaError_t e = fc_launch_kernel_transform_fast(g, p->host_consts, w, V, Vlo, Vlo != nullptr, s,
+                                                                &handled);
+                if (handled) return launch_result(e, "NK1 kernel transform");
+            }
             return launch_result(fc_launch_kernel_transform(g, p->d_consts, w, V, Vlo, Vlo != nullptr, s),
                                  "NK1 kernel transform");
+        }
         case 1: {
             int handled = 0;
             if (!p->generic_transforms) {

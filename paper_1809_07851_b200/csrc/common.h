@@ -66,5 +66,7 @@ cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w,
 int fc_tcgen05_available();
 cudaError_t fc_init_twiddles();
 // compile-time-t transforms; *handled = 0 when t has no specialisation
+cudaError_t fc_launch_kernel_transform_fast(const Geometry &g, const ConvConsts &hc, const float *w, float *V,
+                                            float *Vlo, int split, cudaStream_t s, int *handled);
 cudaError_t fc_launch_transform_fast(const Geometry &g, const ConvConsts &hc, const float *src, float *dst,
                                      int forward, cudaStream_t s, int *handled);

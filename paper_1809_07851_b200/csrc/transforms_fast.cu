@@ -13,6 +13,7 @@
 //
 // Stores of U and loads of X run along the tile index n (lanes = consecutive
 // tiles), so every warp access to the big intermediates is a 128-byte line.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -26,6 +27,73 @@ struct WinoMats {
     float BT[64];
     float AT[64];
 };
+
+// ----------------------------------------------------------- Winograd NK1 ---
+// One thread per (c', c) kernel (lanes along c: coalesced V stores), V = G g G^T
+// fully unrolled for compile-time (t, r); 3xTF32 split written alongside.
+struct GMat {
+    float G[64];
+};
+
+__device__ __forceinline__ float tf32_rna_f(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+template <int T, int R>
+__global__ void __launch_bounds__(256) nk1_wino(Geometry g, GMat gm, const float *__restrict__ w,
+                                                float *__restrict__ V, float *__restrict__ Vlo, int split) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)g.C * g.Cout) return;
+    const int co = (int)(idx / g.C), c = (int)(idx - (long long)co * g.C);
+    const float *ker = w + idx * (R * R);
+    float k[R][R];
+#pragma unroll
+    for (int p = 0; p < R; ++p)
+#pragma unroll
+        for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
+    float tmp[R][T];  // tmp[p][l] = sum_q k[p][q] G[l][q]
+#pragma unroll
+    for (int p = 0; p < R; ++p)
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < R; ++q) s = fmaf(gm.G[l * R + q], k[p][q], s);
+            tmp[p][l] = s;
+        }
+    const size_t zstride = (size_t)g.M * g.Kp;
+    const size_t off = (size_t)co * g.Kp + c;
+    float *vp = V + off, *lp = Vlo ? Vlo + off : nullptr;
+#pragma unroll
+    for (int kk = 0; kk < T; ++kk)
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float s = 0.f;
+#pragma unroll
+            for (int p = 0; p < R; ++p) s = fmaf(gm.G[kk * R + p], tmp[p][l], s);
+            if (split) {
+                const float hi = tf32_rna_f(s);
+                *vp = hi;
+                *lp = s - hi;
+                lp += zstride;
+            } else {
+                *vp = s;
+            }
+            vp += zstride;
+        }
+}
+
+template <int T, int R>
+cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float *w, float *V, float *Vlo,
+                            int split, cudaStream_t s) {
+    GMat gm;
+    for (int i = 0; i < 64; ++i) gm.G[i] = hc.G[i];
+    const long long n = (long long)g.C * g.Cout;
+    nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, gm, w, V, Vlo, split);
+    return cudaGetLastError();
+}
 
 // ----------------------------------------------------------- Winograd NK2 ---
 // One thread per (channel, tile): the t x t input tile straight from global
@@ -425,6 +493,19 @@ cudaError_t fc_init_twiddles() {
     e = cudaMemcpyToSymbol(fct::c_tw, tab, sizeof(tab));
     if (e == cudaSuccess && dev < 64) done_mask |= 1ull << dev;
     return e;
+}
+
+cudaError_t fc_launch_kernel_transform_fast(const Geometry &g, const ConvConsts &hc, const float *w, float *V,
+                                            float *Vlo, int split, cudaStream_t s, int *handled) {
+    *handled = 1;
+    if (g.method == CONV_WINOGRAD) {
+        if (g.t == 4 && g.r == 3) return launch_nk1_wino<4, 3>(g, hc, w, V, Vlo, split, s);
+        if (g.t == 6 && g.r == 3) return launch_nk1_wino<6, 3>(g, hc, w, V, Vlo, split, s);
+        if (g.t == 8 && g.r == 3) return launch_nk1_wino<8, 3>(g, hc, w, V, Vlo, split, s);
+        if (g.t == 6 && g.r == 5) return launch_nk1_wino<6, 5>(g, hc, w, V, Vlo, split, s);
+    }
+    *handled = 0;
+    return cudaSuccess;
 }
 
 cudaError_t fc_launch_transform_fast(const Geometry &g, const ConvConsts &hc, const float *src, float *dst,
