@@ -18,6 +18,7 @@
 
 #include "common.h"
 #include "fft_tile.cuh"
+#include "winograd_tables.h"
 
 using fct::cf;
 
@@ -42,8 +43,9 @@ __device__ __forceinline__ float tf32_rna_f(float x) {
 }
 
 template <int T, int R>
-__global__ void __launch_bounds__(256) nk1_wino(Geometry g, GMat gm, const float *__restrict__ w,
+__global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restrict__ w,
                                                 float *__restrict__ V, float *__restrict__ Vlo, int split) {
+    constexpr wtab::Tables tg = wtab::make(T - R + 1, R);  // G as literals
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (long long)g.C * g.Cout) return;
     const int co = (int)(idx / g.C), c = (int)(idx - (long long)co * g.C);
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, GMat gm, const float
         for (int l = 0; l < T; ++l) {
             float s = 0.f;
 #pragma unroll
-            for (int q = 0; q < R; ++q) s = fmaf(gm.G[l * R + q], k[p][q], s);
+            for (int q = 0; q < R; ++q) s = fmaf((float)tg.G[l][q], k[p][q], s);
             tmp[p][l] = s;
         }
     const size_t zstride = (size_t)g.M * g.Kp;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, GMat gm, const float
         for (int l = 0; l < T; ++l) {
             float s = 0.f;
 #pragma unroll
-            for (int p = 0; p < R; ++p) s = fmaf(gm.G[kk * R + p], tmp[p][l], s);
+            for (int p = 0; p < R; ++p) s = fmaf((float)tg.G[kk][p], tmp[p][l], s);
             if (split) {
                 const float hi = tf32_rna_f(s);
                 *vp = hi;
@@ -88,10 +90,9 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, GMat gm, const float
 template <int T, int R>
 cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float *w, float *V, float *Vlo,
                             int split, cudaStream_t s) {
-    GMat gm;
-    for (int i = 0; i < 64; ++i) gm.G[i] = hc.G[i];
+    (void)hc;
     const long long n = (long long)g.C * g.Cout;
-    nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, gm, w, V, Vlo, split);
+    nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w, V, Vlo, split);
     return cudaGetLastError();
 }
 
@@ -102,8 +103,9 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
 // shared-memory strip-staged variant measured 2.4x slower on VGG-3.2: with the
 // load and compute phases separated by a CTA barrier too few loads stay in flight.)
 template <int T>
-__global__ void __launch_bounds__(128) nk2_wino(Geometry g, WinoMats wm, const float *__restrict__ in,
+__global__ void __launch_bounds__(128) nk2_wino(Geometry g, const float *__restrict__ in,
                                                 float *__restrict__ U) {
+    constexpr wtab::Tables tb = wtab::make(2, T - 1);  // B^T as literals (depends on t only)
     const long long n = (long long)blockIdx.x * 128 + threadIdx.x;
     const int c = blockIdx.y;
     if (n >= g.BN) return;
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(128) nk2_wino(Geometry g, WinoMats wm, const f
         for (int l = 0; l < T; ++l) {
             float s = 0.f;
 #pragma unroll
-            for (int q = 0; q < T; ++q) s = fmaf(wm.BT[l * T + q], d[a][q], s);
+            for (int q = 0; q < T; ++q) s = fmaf((float)tb.BT[l][q], d[a][q], s);
             z[a][l] = s;
         }
     const size_t estride = (size_t)g.K * g.BN_pad;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(128) nk2_wino(Geometry g, WinoMats wm, const f
         for (int l = 0; l < T; ++l) {
             float s = 0.f;
 #pragma unroll
-            for (int a = 0; a < T; ++a) s = fmaf(wm.BT[k * T + a], z[a][l], s);
+            for (int a = 0; a < T; ++a) s = fmaf((float)tb.BT[k][a], z[a][l], s);
             __stcs(dp, s);
             dp += estride;
         }
@@ -154,60 +156,69 @@ __global__ void __launch_bounds__(128) nk2_wino(Geometry g, WinoMats wm, const f
 // loads its t^2 elements of X along n, computes Y = A^T X A, and writes the m x m
 // block into a shared-memory output strip; the CTA then stores the strip's
 // contiguous output rows with coalesced writes (crop to Ho x Wo on the way).
-template <int T>
-__global__ void __launch_bounds__(256, (T <= 6 ? 3 : 2)) nk4_wino(Geometry g, WinoMats wm, int R, int SWo,
+template <int T, int MM>
+__global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, int SWo,
                                                 const float *__restrict__ X, float *__restrict__ out) {
-    extern __shared__ float so[];  // [ntr*m][SWo]
+    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);  // A^T as literals
+    extern __shared__ float so[];  // [img][ntr*m][SWo]
     const int m = g.m;
-    const int i0 = blockIdx.x * R, co = blockIdx.y, b = blockIdx.z;
+    // blockIdx.x = (image group, strip); IPC > 1 only with whole-image strips (R = n_h)
+    const int nstrip = (g.n_h + R - 1) / R;
+    const int strip = blockIdx.x % nstrip, b = (blockIdx.x / nstrip) * IPC, co = blockIdx.y;
+    const int i0 = strip * R;
     const int ntr = min(R, g.n_h - i0);
-    const int ntiles = ntr * g.n_w;
+    const int nimg = min(IPC, g.B - b);
+    const int ntiles = nimg * ntr * g.n_w;  // contiguous in n
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
     const size_t estride = (size_t)g.M * g.BN_pad;
     const float *src0 = X + (size_t)co * g.BN_pad + nbase;
     for (int tl = threadIdx.x; tl < ntiles; tl += blockDim.x) {
-        float x[T][T];
+        // stream the tile row by row: r_k = X[k][:] A (m values), Y += A^T[:, k] r_k,
+        // so only one row of X and the m x m accumulator are live (registers / occupancy)
+        float y[MM][MM];
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int q = 0; q < MM; ++q) y[a][q] = 0.f;
         const float *sp = src0 + tl;
 #pragma unroll
-        for (int k = 0; k < T; ++k)
+        for (int k = 0; k < T; ++k) {
+            float x[T];
 #pragma unroll
             for (int l = 0; l < T; ++l) {
-                x[k][l] = __ldcs(sp);
+                x[l] = __ldcs(sp);
                 sp += estride;
             }
-        const int ti = tl / g.n_w, tj = tl - ti * g.n_w;
-        float *q0 = so + ti * m * SWo + tj * m;
+            if (k & 1) asm volatile("" ::: "memory");  // keep ~2 rows of loads in flight, not all t^2
 #pragma unroll
-        for (int a = 0; a < T - 1; ++a) {
-            if (a >= m) break;
-            float z[T];  // z[l] = sum_k AT[a][k] x[k][l]
+            for (int q = 0; q < MM; ++q) {
+                float rq = 0.f;
 #pragma unroll
-            for (int l = 0; l < T; ++l) {
-                float s = 0.f;
+                for (int l = 0; l < T; ++l) rq = fmaf((float)ta.AT[q][l], x[l], rq);
 #pragma unroll
-                for (int k = 0; k < T; ++k) s = fmaf(wm.AT[a * T + k], x[k][l], s);
-                z[l] = s;
-            }
-#pragma unroll
-            for (int q = 0; q < T - 1; ++q) {
-                if (q >= m) break;
-                float s = 0.f;
-#pragma unroll
-                for (int l = 0; l < T; ++l) s = fmaf(wm.AT[q * T + l], z[l], s);
-                q0[a * SWo + q] = s;
+                for (int a = 0; a < MM; ++a) y[a][q] = fmaf((float)ta.AT[a][k], rq, y[a][q]);
             }
         }
+        const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
+        float *q0 = so + ti * m * SWo + tj * m;
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int q = 0; q < MM; ++q) q0[a * SWo + q] = y[a][q];
     }
     __syncthreads();
     const int y0 = i0 * m;
     const int orows = min(ntr * m, g.Ho - y0);
-    float *dst = out + (((size_t)b * g.Cout + co) * g.Ho + y0) * g.Wo;
-    if (SWo == g.Wo) {
-        for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) __stcs(dst + idx, so[idx]);
-    } else {
-        for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) {
-            const int row = idx / g.Wo, col = idx - row * g.Wo;
-            __stcs(dst + idx, so[row * SWo + col]);
+    for (int im = 0; im < nimg; ++im) {
+        float *dst = out + (((size_t)(b + im) * g.Cout + co) * g.Ho + y0) * g.Wo;
+        const float *src = so + (size_t)im * ntr * m * SWo;
+        if (SWo == g.Wo) {
+            for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) __stcs(dst + idx, src[idx]);
+        } else {
+            for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) {
+                const int row = idx / g.Wo, col = idx - row * g.Wo;
+                __stcs(dst + idx, src[row * SWo + col]);
+            }
         }
     }
 }
@@ -420,24 +431,35 @@ inline int wino_strip_rows(const Geometry &g, int row_floats) {
     return R < g.n_h ? R : g.n_h;
 }
 
-template <int T>
-cudaError_t launch_wino(const Geometry &g, const WinoMats &wm, const float *src, float *dst, bool forward,
-                        cudaStream_t s) {
+template <int T, int MM>
+cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
     if (forward) {
         const unsigned nblk = (unsigned)((g.BN + 127) / 128);
-        nk2_wino<T><<<dim3(nblk, g.C), 128, 0, s>>>(g, wm, src, dst);
+        nk2_wino<T><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
     } else {
+        // about 256 tiles per CTA: strips of one image, or several whole images
         const int SWo = g.n_w * g.m;
-        const int R = wino_strip_rows(g, SWo);
+        static const int target = getenv("FASTCONV_NK4_TILES") ? atoi(getenv("FASTCONV_NK4_TILES")) : 256;
+        int R = wino_strip_rows(g, SWo), IPC = 1;
+        if (R * g.n_w > target) R = target / g.n_w > 0 ? target / g.n_w : 1;
+        if (R >= g.n_h) {
+            R = g.n_h;
+            IPC = target / g.N > 1 ? target / g.N : 1;
+            if (IPC > g.B) IPC = g.B;
+            while (IPC > 1 && (size_t)IPC * R * g.m * SWo * sizeof(float) > 100 * 1024) --IPC;
+        }
         const int nstrip = (g.n_h + R - 1) / R;
-        const size_t smem = sizeof(float) * (size_t)R * g.m * SWo;
+        const int ngroup = (g.B + IPC - 1) / IPC;
+        const size_t smem = sizeof(float) * (size_t)IPC * R * g.m * SWo;
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
         static bool cfg = false;
         if (!cfg) {
-            cudaFuncSetAttribute(nk4_wino<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(nk4_wino<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             cfg = true;
         }
-        nk4_wino<T><<<dim3(nstrip, g.Cout, g.B), 256, smem, s>>>(g, wm, R, SWo, src, dst);
+        const int tiles = IPC * R * g.n_w;
+        const int threads = tiles >= 256 ? 256 : (tiles + 31) / 32 * 32;
+        nk4_wino<T, MM><<<dim3(nstrip * ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
     }
     return cudaGetLastError();
 }
@@ -446,18 +468,14 @@ cudaError_t dispatch(const Geometry &g, const ConvConsts &hc, const float *src, 
                      cudaStream_t s, bool *handled) {
     *handled = true;
     if (g.method == CONV_WINOGRAD) {
-        WinoMats wm;
-        for (int i = 0; i < 64; ++i) {
-            wm.BT[i] = hc.BT[i];
-            wm.AT[i] = hc.AT[i];
-        }
-        switch (g.t) {
-            case 4: return launch_wino<4>(g, wm, src, dst, forward, s);
-            case 5: return launch_wino<5>(g, wm, src, dst, forward, s);
-            case 6: return launch_wino<6>(g, wm, src, dst, forward, s);
-            case 7: return launch_wino<7>(g, wm, src, dst, forward, s);
-            case 8: return launch_wino<8>(g, wm, src, dst, forward, s);
-        }
+        (void)hc;
+        // (t, m) pairs with compile-time matrices; others use the runtime-matrix kernels
+        if (g.t == 4 && g.m == 2) return launch_wino<4, 2>(g, src, dst, forward, s);
+        if (g.t == 4 && g.m == 3) return launch_wino<4, 3>(g, src, dst, forward, s);
+        if (g.t == 5 && g.m == 3) return launch_wino<5, 3>(g, src, dst, forward, s);
+        if (g.t == 6 && g.m == 4) return launch_wino<6, 4>(g, src, dst, forward, s);
+        if (g.t == 6 && g.m == 2) return launch_wino<6, 2>(g, src, dst, forward, s);
+        if (g.t == 8 && g.m == 6) return launch_wino<8, 6>(g, src, dst, forward, s);
         *handled = false;
         return cudaSuccess;
     }
