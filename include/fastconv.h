@@ -88,6 +88,11 @@ typedef struct {
     double alg_bytes[4];
     double alg_flops[4];
     double direct_flops;  /* 2 B C C' Ho Wo r^2 */
+    /* L2-resident batch chunking: conv_forward runs NK1 once, then NK2 -> NK3 -> NK4
+     * for `chunk` images at a time, so U and X of a chunk stay in the 126 MB L2 between
+     * stages.  bytes_U / bytes_X / BN_pad above are per chunk. */
+    int chunk;          /* images per chunk (== B when not chunked) */
+    int nchunks;        /* ceil(B / chunk) */
 } conv_plan_info;
 
 /* Host-only: validate arguments and fill `info` (no CUDA calls).  Errors:
@@ -129,8 +134,8 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
                               void *workspace, size_t workspace_bytes, void *stream);
 
 /* Run a single stage (0 = NK1, 1 = NK2, 2 = NK3, 3 = NK4) on the plan's
- * workspace layout; used by stage-level tests.  Arguments a stage does not
- * read may be NULL. */
+ * workspace layout for the first chunk (images [0, chunk)); used by stage-level
+ * tests.  Arguments a stage does not read may be NULL. */
 conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,
                            void *workspace, size_t workspace_bytes, void *stream);
 
@@ -147,8 +152,24 @@ void conv_destroy(conv_plan_t p);                 /* NULL-safe */
 const char *conv_status_string(conv_status s);    /* static string, never NULL */
 const char *conv_last_error(void);                /* thread-local detail of the last error */
 
-/* Kernel launches one conv_forward issues for this plan (for gpu_launches). */
+/* Kernel launches one conv_forward issues for this plan (for gpu_launches):
+ * 1 + 3 * nchunks (fast methods) or 1 (direct). */
 int conv_forward_launch_count(conv_plan_t p);
+
+/* Per-stage timing without host synchronisation inside a timed loop:
+ * conv_forward_timed() is conv_forward() plus a CUDA event recorded on `stream`
+ * before the first and after every kernel launch (events pre-created by
+ * conv_timer_create: one call consumes launch_count + 1 of the max_launches + 64).  conv_timer_read()
+ * synchronises on the last event and returns, per stage, the sum of the recorded
+ * launch durations in ms (stage_ms[0..3] = NK1..NK4; the direct path reports in
+ * [2]) and the number of launches recorded.  conv_timer_reset() rewinds. */
+typedef struct conv_timer_s *conv_timer_t;
+conv_status conv_timer_create(conv_timer_t *t, int max_launches);
+conv_status conv_forward_timed(conv_plan_t p, const float *in, const float *w, float *out,
+                               void *workspace, size_t workspace_bytes, void *stream, conv_timer_t t);
+conv_status conv_timer_read(conv_timer_t t, float stage_ms[4], int *launches);
+void conv_timer_reset(conv_timer_t t);
+void conv_timer_destroy(conv_timer_t t);   /* NULL-safe */
 
 #ifdef __cplusplus
 }

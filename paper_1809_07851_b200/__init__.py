@@ -43,7 +43,7 @@ class PlanInfo(ctypes.Structure):
                 [(n, ctypes.c_int) for n in ("gemm_Z", "gemm_M", "gemm_K")] +
                 [(n, ctypes.c_size_t) for n in ("bytes_U", "bytes_V", "bytes_X", "workspace_bytes")] +
                 [("alg_bytes", ctypes.c_double * 4), ("alg_flops", ctypes.c_double * 4),
-                 ("direct_flops", ctypes.c_double)])
+                 ("direct_flops", ctypes.c_double), ("chunk", ctypes.c_int), ("nchunks", ctypes.c_int)])
 
     def as_dict(self) -> dict:
         d = {}
@@ -91,6 +91,11 @@ def load(build_if_missing: bool = False):
         "conv_status_string": ([i], ctypes.c_char_p),
         "conv_last_error": ([], ctypes.c_char_p),
         "conv_forward_launch_count": ([vp], i),
+        "conv_timer_create": ([ctypes.POINTER(vp), i], i),
+        "conv_forward_timed": ([vp, vp, vp, vp, vp, sz, vp, vp], i),
+        "conv_timer_read": ([vp, fp, ctypes.POINTER(i)], i),
+        "conv_timer_reset": ([vp], None),
+        "conv_timer_destroy": ([vp], None),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)
@@ -220,6 +225,36 @@ class Plan:
         G = (ctypes.c_double * (t * r))()
         _check(load().conv_plan_winograd_matrices(self._h, AT, BT, G))
         return list(AT), list(BT), list(G)
+
+
+class StageTimer:
+    """conv_timer_*: per-stage CUDA-event timing of conv_forward_timed calls, read once
+    (synchronising) after a timed loop."""
+
+    def __init__(self, max_launches: int):
+        h = ctypes.c_void_p()
+        _check(load().conv_timer_create(ctypes.byref(h), int(max_launches)))
+        self._h = h
+
+    def forward(self, plan: "Plan", x, w, out, workspace, stream=None):
+        _check(load().conv_forward_timed(plan._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                         workspace.data_ptr(), workspace.numel(), _stream_ptr(stream),
+                                         self._h))
+
+    def read(self):
+        ms = (ctypes.c_float * 4)()
+        n = ctypes.c_int()
+        _check(load().conv_timer_read(self._h, ms, ctypes.byref(n)))
+        return list(ms), n.value
+
+    def reset(self):
+        load().conv_timer_reset(self._h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_timer_destroy(h)
+            self._h = None
 
 
 def forward(x: torch.Tensor, w: torch.Tensor, method: str = "winograd", m: int = 4,

@@ -6,10 +6,15 @@
 // (t * ceil((t+1)/2) stored complex numbers = t * (t/2 + 1)), and the stage
 // costs of Table "layer-stuff" P:1008-1042.
 #include <math.h>
+
+#include <cmath>
+#include <vector>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+
+#include <new>
 
 #include "common.h"
 
@@ -149,6 +154,50 @@ conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G
 // ---------------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
+    Geometry c = g;
+    c.B = Bc;
+    c.BN = (long long)Bc * g.N;
+    c.BN_pad = (c.BN + 31) / 32 * 32;
+    return c;
+}
+
+// Optional L2-resident batch chunking: images per chunk so that a chunk's U + X
+// (+ V) could stay in L2 between NK2 -> NK3 -> NK4 (B200: 126 MB L2); among
+// near-maximal chunk sizes prefer the one whose B*N fills whole 256-wide
+// contraction tiles.  OFF by default: on VGG-3.2 (F(4,3)) chunks of 2/4/6/8
+// images measured 2.5x / 1.7x / 1.5x / 1.4x slower than one pass (smaller
+// launches pay wave tails and partial contraction tiles; profiles/r01_notes.md).
+// FASTCONV_CHUNK=<images> forces a chunk size (0 = whole batch);
+// FASTCONV_L2_BUDGET_MB=<MB> enables the budget heuristic.
+static int pick_chunk(const Geometry &G, size_t bytes_V) {
+    if (G.method == CONV_DIRECT) return G.B;
+    const char *env = getenv("FASTCONV_CHUNK");
+    if (env) {
+        const int c = atoi(env);
+        return (c <= 0 || c > G.B) ? G.B : c;
+    }
+    const char *benv = getenv("FASTCONV_L2_BUDGET_MB");
+    if (!benv) return G.B;
+    const double budget = atof(benv) * 1e6;
+    const double per_img = 4.0 * ((double)G.Z * G.K + (double)G.Z * G.M) * G.N;
+    const double avail = budget - (double)bytes_V;
+    long long bmax = avail > per_img ? (long long)(avail / per_img) : 1;
+    if (bmax >= G.B) return G.B;
+    if (bmax < 1) bmax = 1;
+    int best = (int)bmax;
+    double best_eff = 0.0;
+    for (long long bc = bmax; bc >= 1 && bc * 4 >= bmax * 3; --bc) {
+        const double cols = (double)bc * G.N;
+        const double eff = cols / (std::ceil(cols / 256.0) * 256.0);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = (int)bc;
+        }
+    }
+    return best;
+}
+
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
                              Geometry *g, conv_plan_info *info, conv_gemm_impl gemm) {
     if (B < 1 || C < 1 || Cout < 1 || H < 1 || W < 1 || r < 1) {
@@ -223,12 +272,18 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         I.E = G.E; I.planes = G.planes; I.BN = G.BN; I.BN_pad = G.BN_pad;
         I.gemm_Z = G.Z; I.gemm_M = G.M; I.gemm_K = G.K;
         I.direct_flops = 2.0 * B * (double)C * Cout * G.Ho * G.Wo * r * r;
+        I.chunk = B;
+        I.nchunks = 1;
         if (method != CONV_DIRECT) {
             const int split = (gemm != CONV_GEMM_FFMA);
-            I.bytes_U = (size_t)G.Z * G.K * G.BN_pad * 4;
             const size_t vb = (size_t)G.Z * G.M * G.Kp * 4;  // V_hi, then V_lo at the next 256 B boundary
             I.bytes_V = split ? align256(vb) + vb : vb;
-            I.bytes_X = (size_t)G.Z * G.M * G.BN_pad * 4;
+            I.chunk = pick_chunk(G, I.bytes_V);
+            I.nchunks = (B + I.chunk - 1) / I.chunk;
+            const Geometry Gc = fc_chunk_geometry(G, I.chunk);
+            I.BN_pad = Gc.BN_pad;
+            I.bytes_U = (size_t)G.Z * G.K * Gc.BN_pad * 4;
+            I.bytes_X = (size_t)G.Z * G.M * Gc.BN_pad * 4;
             I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
             // Table layer-stuff, c=C, c'=C', alpha=1; wE = reals per tile
             const double wE = (double)G.planes * G.E * (method == CONV_WINOGRAD ? 1 : 1);
@@ -355,6 +410,8 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
         p->ws_bytes = p->info.workspace_bytes;
         if (gemm == CONV_GEMM_FFMA) p->off_Vlo = 0;
     }
+    p->chunk = p->info.chunk;
+    p->nchunks = p->info.nchunks;
     *out = p;
     return CONV_OK;
 }
@@ -416,7 +473,7 @@ conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, d
 
 int conv_forward_launch_count(conv_plan_t p) {
     if (!p) return 0;
-    return p->g.method == CONV_DIRECT ? 1 : 4;
+    return p->g.method == CONV_DIRECT ? 1 : 1 + 3 * p->nchunks;
 }
 
 // -- pointer checks ----------------------------------------------------------
@@ -469,9 +526,8 @@ static conv_status launch_result(cudaError_t e, const char *what) {
     return CONV_OK;
 }
 
-static conv_status run_stage(conv_plan_s *p, int stage, const float *in, const float *w, float *out,
-                             char *ws, cudaStream_t s) {
-    const Geometry &g = p->g;
+static conv_status run_stage(conv_plan_s *p, const Geometry &g, int stage, const float *in, const float *w,
+                             float *out, char *ws, cudaStream_t s) {
     float *V = (float *)(ws + p->off_V);
     float *Vlo = p->gemm == CONV_GEMM_FFMA ? nullptr : (float *)(ws + p->off_Vlo);
     float *U = (float *)(ws + p->off_U);
@@ -533,17 +589,52 @@ static conv_status check_forward_args(conv_plan_s *p, const float *in, const flo
     return CONV_OK;
 }
 
+}  // extern "C"
+
+struct conv_timer_s {
+    std::vector<cudaEvent_t> ev;  // ev[i] recorded after launch i-1 (ev[0]: before the first)
+    std::vector<int> stage;       // stage of the launch ending at ev[i]; -1 = start marker
+    int used = 0;
+};
+
+// The whole forward pass: NK1 once (V does not depend on the batch), then
+// NK2 -> NK3 -> NK4 per chunk of images so U and X stay L2-resident.
+static conv_status forward_impl(conv_plan_s *p, const float *in, const float *w, float *out, char *ws,
+                                cudaStream_t s, conv_timer_s *t) {
+    auto mark = [&](int stage) -> conv_status {
+        if (!t) return CONV_OK;
+        if (t->used >= (int)t->ev.size()) {
+            fc_set_error("conv_timer capacity exceeded");
+            return CONV_ERR_INVALID_ARG;
+        }
+        t->stage[t->used] = stage;
+        return launch_result(cudaEventRecord(t->ev[t->used++], s), "cudaEventRecord");
+    };
+    conv_status st = mark(-1);
+    if (st) return st;
+    const Geometry &g = p->g;
+    if (g.method == CONV_DIRECT) {
+        st = launch_result(fc_launch_direct(g, in, w, out, s), "NK5 direct");
+        return st ? st : mark(2);
+    }
+    if ((st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0))) return st;
+    for (int b0 = 0; b0 < g.B; b0 += p->chunk) {
+        const Geometry gc = fc_chunk_geometry(g, g.B - b0 < p->chunk ? g.B - b0 : p->chunk);
+        const float *in_c = in + (size_t)b0 * g.C * g.H * g.W;
+        float *out_c = out + (size_t)b0 * g.Cout * g.Ho * g.Wo;
+        for (int k = 1; k < 4; ++k)
+            if ((st = run_stage(p, gc, k, in_c, w, out_c, ws, s)) || (st = mark(k))) return st;
+    }
+    return CONV_OK;
+}
+
+extern "C" {
+
 conv_status conv_forward(conv_plan_t p, const float *in, const float *w, float *out, void *ws,
                          size_t ws_bytes, void *stream) {
     conv_status st = check_forward_args(p, in, w, out, ws, ws_bytes);
     if (st) return st;
-    cudaStream_t s = (cudaStream_t)stream;
-    if (p->g.method == CONV_DIRECT) return launch_result(fc_launch_direct(p->g, in, w, out, s), "NK5 direct");
-    for (int k = 0; k < 4; ++k) {
-        st = run_stage(p, k, in, w, out, (char *)ws, s);
-        if (st) return st;
-    }
-    return CONV_OK;
+    return forward_impl(p, in, w, out, (char *)ws, (cudaStream_t)stream, nullptr);
 }
 
 conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,
@@ -566,7 +657,72 @@ conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const floa
     if (stage == 0 && (st = check_dev_ptr(p, w, "weights"))) return st;
     if (stage == 1 && (st = check_dev_ptr(p, in, "in"))) return st;
     if (stage == 3 && (st = check_dev_ptr(p, out, "out"))) return st;
-    return run_stage(p, stage, in, w, out, (char *)ws, (cudaStream_t)stream);
+    const Geometry g0 = stage == 0 ? p->g : fc_chunk_geometry(p->g, p->chunk);
+    return run_stage(p, g0, stage, in, w, out, (char *)ws, (cudaStream_t)stream);
+}
+
+conv_status conv_timer_create(conv_timer_t *t, int max_launches) {
+    if (!t || max_launches < 1) {
+        fc_set_error("bad timer arguments");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_timer_s *tm = new (std::nothrow) conv_timer_s();
+    if (!tm) return CONV_ERR_OUT_OF_MEMORY;
+    tm->ev.resize((size_t)max_launches + 64);
+    tm->stage.assign(tm->ev.size(), -1);
+    for (size_t i = 0; i < tm->ev.size(); ++i) {
+        if (cudaEventCreate(&tm->ev[i]) != cudaSuccess) {
+            for (size_t j = 0; j < i; ++j) cudaEventDestroy(tm->ev[j]);
+            delete tm;
+            return launch_result(cudaGetLastError(), "cudaEventCreate");
+        }
+    }
+    *t = tm;
+    return CONV_OK;
+}
+
+void conv_timer_reset(conv_timer_t t) {
+    if (t) t->used = 0;
+}
+
+void conv_timer_destroy(conv_timer_t t) {
+    if (!t) return;
+    for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
+    delete t;
+}
+
+conv_status conv_forward_timed(conv_plan_t p, const float *in, const float *w, float *out, void *ws,
+                               size_t ws_bytes, void *stream, conv_timer_t t) {
+    if (!t) {
+        fc_set_error("NULL timer");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_status st = check_forward_args(p, in, w, out, ws, ws_bytes);
+    if (st) return st;
+    return forward_impl(p, in, w, out, (char *)ws, (cudaStream_t)stream, t);
+}
+
+conv_status conv_timer_read(conv_timer_t t, float stage_ms[4], int *launches) {
+    if (!t || !stage_ms) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    for (int k = 0; k < 4; ++k) stage_ms[k] = 0.f;
+    int n = 0;
+    if (t->used > 0) {
+        cudaError_t e = cudaEventSynchronize(t->ev[t->used - 1]);
+        if (e != cudaSuccess) return launch_result(e, "cudaEventSynchronize");
+    }
+    for (int i = 1; i < t->used; ++i) {
+        if (t->stage[i] < 0) continue;  // start marker of the next forward call
+        float ms = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&ms, t->ev[i - 1], t->ev[i]);
+        if (e != cudaSuccess) return launch_result(e, "cudaEventElapsedTime");
+        stage_ms[t->stage[i]] += ms;
+        ++n;
+    }
+    if (launches) *launches = n;
+    return CONV_OK;
 }
 
 conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w, float *out,
@@ -577,33 +733,11 @@ conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w
         fc_set_error("NULL stage_ms");
         return CONV_ERR_INVALID_ARG;
     }
-    cudaStream_t s = (cudaStream_t)stream;
-    cudaEvent_t ev[5];
-    for (int i = 0; i < 5; ++i) {
-        if (cudaEventCreate(&ev[i]) != cudaSuccess) {
-            for (int j = 0; j < i; ++j) cudaEventDestroy(ev[j]);
-            return launch_result(cudaGetLastError(), "cudaEventCreate");
-        }
-    }
-    for (int k = 0; k < 4; ++k) stage_ms[k] = 0.f;
-    cudaEventRecord(ev[0], s);
-    if (p->g.method == CONV_DIRECT) {
-        st = launch_result(fc_launch_direct(p->g, in, w, out, s), "NK5 direct");
-        cudaEventRecord(ev[1], s);
-        cudaEventSynchronize(ev[1]);
-        if (!st) cudaEventElapsedTime(&stage_ms[2], ev[0], ev[1]);
-    } else {
-        for (int k = 0; k < 4 && !st; ++k) {
-            st = run_stage(p, k, in, w, out, (char *)ws, s);
-            cudaEventRecord(ev[k + 1], s);
-        }
-        cudaEventSynchronize(ev[4]);
-        if (!st)
-            for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&stage_ms[k], ev[k], ev[k + 1]);
-    }
-    cudaError_t e = cudaGetLastError();
-    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
-    if (!st && e != cudaSuccess) st = launch_result(e, "profiled forward");
+    conv_timer_t t = nullptr;
+    if ((st = conv_timer_create(&t, conv_forward_launch_count(p)))) return st;
+    st = forward_impl(p, in, w, out, (char *)ws, (cudaStream_t)stream, t);
+    if (!st) st = conv_timer_read(t, stage_ms, nullptr);
+    conv_timer_destroy(t);
     return st;
 }
 

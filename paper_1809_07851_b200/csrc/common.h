@@ -41,8 +41,12 @@ struct conv_plan_s {
     ConvConsts *d_consts;                 // device copy
     int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
+    int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
     conv_plan_info info;
 };
+
+// geometry of a chunk of Bc images (U / X row pitch BN_pad follows the chunk)
+Geometry fc_chunk_geometry(const Geometry &g, int Bc);
 
 // ---- host helpers (plan.cu) ----
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,

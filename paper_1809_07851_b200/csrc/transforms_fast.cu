@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128) nk2_wino(Geometry g, const float *__restr
             float s = 0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) s = fmaf((float)tb.BT[k][a], z[a][l], s);
-            __stcs(dp, s);
+            *dp = s;  // plain store: U of an L2-resident chunk is re-read by NK3 from L2
             dp += estride;
         }
 }
@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
 #pragma unroll
             for (int k = 0; k < T; ++k) {
                 const size_t e = (size_t)(k * H + l) * estride;
-                __stcs(d0 + e, z[k].x);
-                __stcs(d1 + e, z[k].y);
+                d0[e] = z[k].x;
+                d1[e] = z[k].y;
             }
         } else {  // Gauss: (U_r + U_i, U_r, U_i) in planes 0, 1, 2
             float *d0 = U + (size_t)c * g.BN_pad + n;
@@ -307,9 +307,9 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
 #pragma unroll
             for (int k = 0; k < T; ++k) {
                 const size_t e = (size_t)(k * H + l) * estride;
-                __stcs(d0 + e, z[k].x + z[k].y);
-                __stcs(d0 + pl + e, z[k].x);
-                __stcs(d0 + 2 * pl + e, z[k].y);
+                d0[e] = z[k].x + z[k].y;
+                d0[pl + e] = z[k].x;
+                d0[2 * pl + e] = z[k].y;
             }
         }
     }

@@ -235,3 +235,20 @@ def test_forward_host_and_profiled():
     assert rel_err(ho.numpy().astype(np.float64), O) <= 1e-5
     ms = p.forward_profiled(di, dw, do, ws)
     assert len(ms) == 4 and all(v >= 0 for v in ms)
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 0])
+@pytest.mark.parametrize("method,m", [("winograd", 4), ("winograd", 6), ("regular_fft", 8), ("gauss_fft", 5)])
+def test_l2_chunking(method, m, chunk, monkeypatch):
+    """conv_forward processes the batch in L2-resident chunks of images (ragged last chunk);
+    the result must not depend on the chunking."""
+    cfg = synth.custom(7, 24, 40, 22, 19, 3, seed=51, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    monkeypatch.setenv("FASTCONV_CHUNK", str(chunk))
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+    assert p.info["chunk"] == (chunk if chunk else cfg.B)
+    assert p.launches == 1 + 3 * p.info["nchunks"]
+    y = p.forward(I.cuda(), W.cuda())
+    torch.cuda.synchronize()
+    assert rel_err(y.cpu().double().numpy(), O) <= tol(method, m, cfg.r)
