@@ -115,12 +115,6 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
           "=r"(v[30]), "=r"(v[31])                                                                                \
         : "r"(taddr))
 
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
 struct TileCoord {
     int z, m0, n0;
 };

@@ -103,10 +103,10 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
 // shared-memory strip-staged variant measured 2.4x slower on VGG-3.2: with the
 // load and compute phases separated by a CTA barrier too few loads stay in flight.)
 template <int T>
-__global__ void __launch_bounds__(128) nk2_wino(Geometry g, const float *__restrict__ in,
+__global__ void __launch_bounds__(512) nk2_wino(Geometry g, const float *__restrict__ in,
                                                 float *__restrict__ U) {
     constexpr wtab::Tables tb = wtab::make(2, T - 1);  // B^T as literals (depends on t only)
-    const long long n = (long long)blockIdx.x * 128 + threadIdx.x;
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
     if (n >= g.BN) return;
     const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
@@ -150,6 +150,72 @@ __global__ void __launch_bounds__(128) nk2_wino(Geometry g, const float *__restr
         }
 }
 
+
+// Two horizontally adjacent tiles per thread (even n_w): the 2-tile window
+// (m + t columns) is read with 8-byte vector loads (x0 = 2pm is even) and the
+// two results of every transformed element are written as one float2 at
+// (n, n+1) -- half the load/store instructions of one tile per thread.
+template <int T, int MM>
+__global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__restrict__ in,
+                                                     float *__restrict__ U) {
+    constexpr wtab::Tables tb = wtab::make(2, T - 1);
+    constexpr int WID = MM + T;  // columns covered by the two tiles
+    const long long pidx = (long long)blockIdx.x * 128 + threadIdx.x;
+    const int c = blockIdx.y;
+    const long long n = 2 * pidx;
+    if (n >= g.BN) return;
+    const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
+    const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+    const int y0 = ti * MM, x0 = tj * MM;
+    const float *src = in + ((size_t)b * g.C + c) * g.H * g.W + (size_t)y0 * g.W + x0;
+    const bool interior = (y0 + T <= g.H) && (x0 + WID <= g.W);
+    const bool vec = interior && ((g.W & 1) == 0);
+    float zA[T][T], zB[T][T];
+#pragma unroll
+    for (int a = 0; a < T; ++a) {
+        float d[WID];
+        if (vec) {
+            const float2 *r2 = reinterpret_cast<const float2 *>(src + a * g.W);
+#pragma unroll
+            for (int q = 0; q < WID / 2; ++q) {
+                const float2 v = __ldg(r2 + q);
+                d[2 * q] = v.x;
+                d[2 * q + 1] = v.y;
+            }
+            if (WID & 1) d[WID - 1] = __ldg(src + a * g.W + WID - 1);
+        } else {
+#pragma unroll
+            for (int q = 0; q < WID; ++q)
+                d[q] = (y0 + a < g.H && x0 + q < g.W) ? __ldg(src + a * g.W + q) : 0.f;
+        }
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float sa = 0.f, sb = 0.f;
+#pragma unroll
+            for (int q = 0; q < T; ++q) {
+                sa = fmaf((float)tb.BT[l][q], d[q], sa);
+                sb = fmaf((float)tb.BT[l][q], d[MM + q], sb);
+            }
+            zA[a][l] = sa;
+            zB[a][l] = sb;
+        }
+    }
+    const size_t estride = (size_t)g.K * g.BN_pad;
+    float *dp = U + (size_t)c * g.BN_pad + n;
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+#pragma unroll
+        for (int l = 0; l < T; ++l) {
+            float sa = 0.f, sb = 0.f;
+#pragma unroll
+            for (int a = 0; a < T; ++a) {
+                sa = fmaf((float)tb.BT[k][a], zA[a][l], sa);
+                sb = fmaf((float)tb.BT[k][a], zB[a][l], sb);
+            }
+            *reinterpret_cast<float2 *>(dp) = make_float2(sa, sb);
+            dp += estride;
+        }
+}
 
 // ----------------------------------------------------------- Winograd NK4 ---
 // CTA = (strip of R tile rows, output channel c', image b).  One thread per tile
@@ -316,55 +382,59 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
 }
 
 // ---------------------------------------------------------------- FFT NK4 ---
+// CTA = R tile rows of IPC consecutive images (their tiles are contiguous in n).
+// Phase A: one (half-spectrum column l, tile) per thread -- load the t values of
+// X along n (Gauss: T1-T3, T1+T2 on load), inverse FFT along the tile's H axis,
+// keep the m output rows in shared memory.  Phase B: two output rows per complex
+// inverse FFT (A + iB packing, self-conjugate bins' imaginary parts dropped,
+// reading R7), cropped m x m block into a shared-memory output strip.  Phase C:
+// coalesced streaming stores of each image's output rows.
 template <int T>
-__global__ void __launch_bounds__(256) nk4_fft(Geometry g, const float *__restrict__ X, float *__restrict__ out) {
+__global__ void __launch_bounds__(512) nk4_fft(Geometry g, int R, int IPC, int SWo, const float *__restrict__ X,
+                                               float *__restrict__ out) {
     constexpr int H = FftCfg<T>::H;
     const int m = g.m;
     const int S = (m * H) % 2 ? m * H : m * H + 1;
-    extern __shared__ float2 zs[];  // [FTN][S]: tile nn, output row a < m, bin l
-    const int co = blockIdx.y;
-    const long long n0 = (long long)blockIdx.x * FTN;
+    const int nstrip = (g.n_h + R - 1) / R;
+    const int strip = blockIdx.x % nstrip, b = (blockIdx.x / nstrip) * IPC, co = blockIdx.y;
+    const int i0 = strip * R;
+    const int ntr = min(R, g.n_h - i0);
+    const int nimg = min(IPC, g.B - b);
+    const int ntiles = nimg * ntr * g.n_w;
+    const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
+    extern __shared__ float2 zs[];                                     // [ntiles][S]
+    float *so = reinterpret_cast<float *>(zs + (size_t)IPC * R * g.n_w * S);  // [nimg*ntr*m][SWo]
     const size_t estride = (size_t)g.M * g.BN_pad;
-    for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
-        const int nn = it % FTN, l = it / FTN;
-        const long long n = n0 + nn;
+    const size_t hstride = (size_t)H * estride;  // k -> k+1 along the element index e = k*H + l
+    for (int it = threadIdx.x; it < H * ntiles; it += blockDim.x) {
+        const int tl = it % ntiles, l = it / ntiles;
         cf z[T];
-        if (n < g.BN) {
-            const float *s0 = X + (size_t)co * g.BN_pad + n;
-            if (g.method == CONV_REGULAR_FFT) {
-                const float *s1 = X + (size_t)(g.Cout + co) * g.BN_pad + n;
+        const float *s0 = X + (size_t)co * g.BN_pad + nbase + tl + (size_t)l * estride;
+        if (g.method == CONV_REGULAR_FFT) {
+            const float *s1 = s0 + (size_t)g.Cout * g.BN_pad;
 #pragma unroll
-                for (int k = 0; k < T; ++k) {
-                    const size_t e = (size_t)(k * H + l) * estride;
-                    z[k] = cf{__ldcs(s0 + e), __ldcs(s1 + e)};
-                }
-            } else {  // Gauss: Re = T1 - T3, Im = T1 + T2
-                const size_t pl = (size_t)g.E * estride;
+            for (int k = 0; k < T; ++k) z[k] = cf{__ldcs(s0 + k * hstride), __ldcs(s1 + k * hstride)};
+        } else {  // Gauss: Re = T1 - T3, Im = T1 + T2
+            const size_t pl = (size_t)g.E * estride;
 #pragma unroll
-                for (int k = 0; k < T; ++k) {
-                    const size_t e = (size_t)(k * H + l) * estride;
-                    const float t1 = __ldcs(s0 + e), t2 = __ldcs(s0 + pl + e), t3 = __ldcs(s0 + 2 * pl + e);
-                    z[k] = cf{t1 - t3, t1 + t2};
-                }
+            for (int k = 0; k < T; ++k) {
+                const float *p = s0 + k * hstride;
+                const float t1 = __ldcs(p), t2 = __ldcs(p + pl), t3 = __ldcs(p + 2 * pl);
+                z[k] = cf{t1 - t3, t1 + t2};
             }
-        } else {
-#pragma unroll
-            for (int k = 0; k < T; ++k) z[k] = cf{0.f, 0.f};
         }
         fct::fft<T, +1>(z);  // inverse along the tile's H axis (unnormalised; 1/t^2 sits in V)
-        float2 *dst = zs + nn * S + l;
+        float2 *dst = zs + (size_t)tl * S + l;
 #pragma unroll
         for (int a = 0; a < T; ++a)
             if (a < m) dst[a * H] = make_float2(z[a].x, z[a].y);
     }
     __syncthreads();
     const int RP = (m + 1) / 2;
-    for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
-        const int nn = it % FTN, p = it / FTN;
+    for (int it = threadIdx.x; it < RP * ntiles; it += blockDim.x) {
+        const int tl = it % ntiles, p = it / ntiles;
         const int a0 = 2 * p, a1 = 2 * p + 1;
-        const long long n = n0 + nn;
-        if (n >= g.BN) continue;
-        const float2 *ra = zs + nn * S + a0 * H;
+        const float2 *ra = zs + (size_t)tl * S + a0 * H;
         const float2 *rb = ra + H;
         const bool has1 = a1 < m;
         cf z[T];
@@ -376,21 +446,29 @@ __global__ void __launch_bounds__(256) nk4_fft(Geometry g, const float *__restri
                 A.y = 0.f;
                 Bv.y = 0.f;
             }
-            z[l] = cf{A.x - Bv.y, A.y + Bv.x};                       // A + i B
+            z[l] = cf{A.x - Bv.y, A.y + Bv.x};                               // A + i B
             if (l > 0 && 2 * l < T) z[T - l] = cf{A.x + Bv.y, Bv.x - A.y};  // conj(A) + i conj(B)
         }
         fct::fft<T, +1>(z);
-        const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
-        const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
-        const int y0 = ti * m + a0, x0 = tj * m;
-        float *d0 = out + ((size_t)b * g.Cout + co) * g.Ho * g.Wo + (size_t)y0 * g.Wo + x0;
-        const bool w0 = y0 < g.Ho, w1 = has1 && (y0 + 1 < g.Ho);
+        const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts tile rows across the CTA's images
+        float *q0 = so + (size_t)(ti * m + a0) * SWo + tj * m;
 #pragma unroll
         for (int q = 0; q < T; ++q) {
-            if (q < m && x0 + q < g.Wo) {
-                if (w0) d0[q] = z[q].x;
-                if (w1) d0[g.Wo + q] = z[q].y;
+            if (q < m) {
+                q0[q] = z[q].x;
+                if (has1) q0[SWo + q] = z[q].y;
             }
+        }
+    }
+    __syncthreads();
+    const int y0 = i0 * m;
+    const int orows = min(ntr * m, g.Ho - y0);
+    for (int im = 0; im < nimg; ++im) {
+        float *dst = out + (((size_t)(b + im) * g.Cout + co) * g.Ho + y0) * g.Wo;
+        const float *src = so + (size_t)im * ntr * m * SWo;
+        for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) {
+            const int row = idx / g.Wo, col = idx - row * g.Wo;
+            __stcs(dst + idx, src[row * SWo + col]);
         }
     }
 }
@@ -408,15 +486,34 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         }
         nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst);
     } else {
+        // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
+        // whole images when they fit (IPC images), else strips of R tile rows
         const int Sm = (g.m * H) % 2 ? g.m * H : g.m * H + 1;
-        const size_t smem = sizeof(float2) * FTN * Sm;
+        const int SWo = g.n_w * g.m;
+        auto smem_of = [&](int ipc, int r) {
+            return (size_t)ipc * r * g.n_w * Sm * sizeof(float2) + (size_t)ipc * r * g.m * SWo * sizeof(float);
+        };
+        const int target = 512 / H > 1 ? 512 / H : 1;
+        int R = target / g.n_w > 0 ? target / g.n_w : 1, IPC = 1;
+        if (R >= g.n_h) {
+            R = g.n_h;
+            IPC = target / g.N > 1 ? target / g.N : 1;
+            if (IPC > g.B) IPC = g.B;
+        }
+        while (IPC > 1 && smem_of(IPC, R) > 100 * 1024) --IPC;
+        while (R > 1 && smem_of(IPC, R) > 100 * 1024) --R;
+        const size_t smem = smem_of(IPC, R);
+        if (smem > 200 * 1024) return cudaErrorInvalidValue;
         static bool cfg = false;
         if (!cfg) {
-            cudaFuncSetAttribute(nk4_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(float2) * FTN * FftCfg<T>::S2));
+            cudaFuncSetAttribute(nk4_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             cfg = true;
         }
-        nk4_fft<T><<<dim3(nblk, g.Cout), 256, smem, s>>>(g, src, dst);
+        const int nstrip = (g.n_h + R - 1) / R;
+        const int ngroup = (g.B + IPC - 1) / IPC;
+        const int items = H * IPC * R * g.n_w;
+        const int threads = items >= 512 ? 512 : (items + 31) / 32 * 32;
+        nk4_fft<T><<<dim3(nstrip * ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
     }
     return cudaGetLastError();
 }
@@ -434,8 +531,15 @@ inline int wino_strip_rows(const Geometry &g, int row_floats) {
 template <int T, int MM>
 cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
     if (forward) {
-        const unsigned nblk = (unsigned)((g.BN + 127) / 128);
-        nk2_wino<T><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
+        static const int no_pair = getenv("FASTCONV_NK2_PAIR") == nullptr;
+        if (g.n_w % 2 == 0 && !no_pair) {
+            const unsigned nblk = (unsigned)((g.BN / 2 + 127) / 128);
+            nk2_wino_pair<T, MM><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
+        } else {
+            static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
+            const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
+            nk2_wino<T><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst);
+        }
     } else {
         // about 256 tiles per CTA: strips of one image, or several whole images
         const int SWo = g.n_w * g.m;
