@@ -133,6 +133,17 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
                               float *d_in, float *d_w, float *d_out,
                               void *workspace, size_t workspace_bytes, void *stream);
 
+/* Inference with cached weight transforms: the kernel
+ * transform V depends only on the weights, so conv_transform_weights() runs NK1
+ * once into the V region of `workspace`, and every later conv_forward_cached()
+ * runs NK2 -> NK3 -> NK4 only, reading that V.  The workspace must keep its V
+ * region intact between the calls (U / X are overwritten as usual).  Same
+ * results as conv_forward, bit for bit. */
+conv_status conv_transform_weights(conv_plan_t p, const float *w, void *workspace, size_t workspace_bytes,
+                                   void *stream);
+conv_status conv_forward_cached(conv_plan_t p, const float *in, float *out, void *workspace,
+                                size_t workspace_bytes, void *stream);
+
 /* Run a single stage (0 = NK1, 1 = NK2, 2 = NK3, 3 = NK4) on the plan's
  * workspace layout for the first chunk (images [0, chunk)); used by stage-level
  * tests.  Arguments a stage does not read may be NULL. */

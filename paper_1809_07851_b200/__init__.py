@@ -91,6 +91,8 @@ def load(build_if_missing: bool = False):
         "conv_status_string": ([i], ctypes.c_char_p),
         "conv_last_error": ([], ctypes.c_char_p),
         "conv_forward_launch_count": ([vp], i),
+        "conv_transform_weights": ([vp, vp, vp, sz, vp], i),
+        "conv_forward_cached": ([vp, vp, vp, vp, sz, vp], i),
         "conv_timer_create": ([ctypes.POINTER(vp), i], i),
         "conv_forward_timed": ([vp, vp, vp, vp, vp, sz, vp, vp], i),
         "conv_timer_read": ([vp, fp, ctypes.POINTER(i)], i),
@@ -196,6 +198,22 @@ class Plan:
         _check(load().conv_forward(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
                                    workspace.data_ptr(), workspace.numel() * workspace.element_size(),
                                    _stream_ptr(stream)))
+        return out
+
+    def transform_weights(self, w, workspace, stream=None):
+        """NK1 once into the workspace's V region (conv_transform_weights)."""
+        _check_tensor(w, "weights", self.w_shape)
+        _check(load().conv_transform_weights(self._h, w.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                             _stream_ptr(stream)))
+
+    def forward_cached(self, x, workspace, out=None, stream=None) -> torch.Tensor:
+        """NK2 -> NK3 -> NK4 against the V left in `workspace` by transform_weights."""
+        _check_tensor(x, "input", self.in_shape)
+        if out is None:
+            out = torch.empty(self.out_shape, dtype=torch.float32, device=x.device)
+        _check_tensor(out, "out", self.out_shape)
+        _check(load().conv_forward_cached(self._h, x.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                          workspace.numel(), _stream_ptr(stream)))
         return out
 
     def forward_profiled(self, x, w, out, workspace, stream=None):

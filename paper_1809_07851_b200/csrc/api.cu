@@ -600,7 +600,7 @@ struct conv_timer_s {
 // The whole forward pass: NK1 once (V does not depend on the batch), then
 // NK2 -> NK3 -> NK4 per chunk of images so U and X stay L2-resident.
 static conv_status forward_impl(conv_plan_s *p, const float *in, const float *w, float *out, char *ws,
-                                cudaStream_t s, conv_timer_s *t) {
+                                cudaStream_t s, conv_timer_s *t, bool skip_nk1 = false) {
     auto mark = [&](int stage) -> conv_status {
         if (!t) return CONV_OK;
         if (t->used >= (int)t->ev.size()) {
@@ -617,7 +617,7 @@ static conv_status forward_impl(conv_plan_s *p, const float *in, const float *w,
         st = launch_result(fc_launch_direct(g, in, w, out, s), "NK5 direct");
         return st ? st : mark(2);
     }
-    if ((st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0))) return st;
+    if (!skip_nk1 && ((st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0)))) return st;
     for (int b0 = 0; b0 < g.B; b0 += p->chunk) {
         const Geometry gc = fc_chunk_geometry(g, g.B - b0 < p->chunk ? g.B - b0 : p->chunk);
         const float *in_c = in + (size_t)b0 * g.C * g.H * g.W;
@@ -635,6 +635,48 @@ conv_status conv_forward(conv_plan_t p, const float *in, const float *w, float *
     conv_status st = check_forward_args(p, in, w, out, ws, ws_bytes);
     if (st) return st;
     return forward_impl(p, in, w, out, (char *)ws, (cudaStream_t)stream, nullptr);
+}
+
+conv_status conv_transform_weights(conv_plan_t p, const float *w, void *ws, size_t ws_bytes, void *stream) {
+    if (!p) {
+        fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->g.method == CONV_DIRECT) {
+        fc_set_error("direct plans have no kernel transform");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    conv_status st = check_device(p);
+    if (st) return st;
+    if ((st = check_dev_ptr(p, w, "weights"))) return st;
+    if (ws_bytes < p->ws_bytes) {
+        fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if ((st = check_dev_ptr(p, ws, "workspace"))) return st;
+    return run_stage(p, p->g, 0, nullptr, w, nullptr, (char *)ws, (cudaStream_t)stream);
+}
+
+conv_status conv_forward_cached(conv_plan_t p, const float *in, float *out, void *ws, size_t ws_bytes,
+                                void *stream) {
+    if (!p) {
+        fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->g.method == CONV_DIRECT) {
+        fc_set_error("direct plans have no transformed weights");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    conv_status st = check_device(p);
+    if (st) return st;
+    if ((st = check_dev_ptr(p, in, "in"))) return st;
+    if ((st = check_dev_ptr(p, out, "out"))) return st;
+    if (ws_bytes < p->ws_bytes) {
+        fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if ((st = check_dev_ptr(p, ws, "workspace"))) return st;
+    return forward_impl(p, in, nullptr, out, (char *)ws, (cudaStream_t)stream, nullptr, true);
 }
 
 conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,

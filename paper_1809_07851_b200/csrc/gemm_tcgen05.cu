@@ -5,22 +5,28 @@
 //     X_z [M x BN] = V_z [M x K] . U_z [K x BN]        z < Z
 //
 // computed in fp32 semantics with a 3xTF32 split (reading R11):
-// a = a_hi + a_lo with a_hi = rna_tf32(a), a_lo = a - a_hi, and
-//     V.U ~= V_lo.U_hi + V_hi.U_lo + V_hi.U_hi      (fp32 TMEM accumulation).
-// V_hi / V_lo are pre-split by NK1 (V is small); the U tile is split in shared
-// memory by four "splitter" warps between the TMA load and the MMA, so U is
-// read from HBM exactly once per CTA tile and never stored twice.
+//     V.U ~= V_lo.U_hi + V_hi.U_lo + V_hi.U_hi      (fp32 TMEM accumulation),
+// V_hi = rna_tf32(V), V_lo = V - V_hi pre-split by NK1 (V is small); the MMA
+// reads U truncated to TF32 (measured, dbg/mma_test.cu), so U_hi = U and four
+// "splitter" warps write U_lo = U - trunc_tf32(U) next to the TMA-loaded U tile:
+// U is read from HBM exactly once per tile and never stored twice.
 //
-// Kernel anatomy (persistent, warp-specialised, one CTA per SM):
-//   warp 0      TMA producer: V_hi, V_lo (K-major, 128B swizzle) and U
-//               (MN-major, 128B swizzle with 32B atoms -- the only MN-major
-//               swizzle tcgen05 accepts for 32-bit operands) into a smem ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
-//               M=128 x N=BLOCK_N x K=8, D in TMEM, double-buffered)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> global X
-//   warps 8-11  splitter: U -> (rna(U), U - rna(U)) in smem, fence.proxy.async
-// mbarriers: full (TMA tx), split (splitter done), empty (MMA commit),
-// tmem_full (MMA commit), tmem_empty (epilogue drained).
+// One persistent, warp-specialised kernel, CG = 1 (one CTA, M = 128) or CG = 2
+// (a CTA pair / cluster of 2 issuing cta_group::2 MMAs with M = 256: rank r
+// holds V rows [128 r, 128 r + 128) and U columns [r N/2, (r+1) N/2); each
+// CTA's TMEM receives its 128 rows x N columns):
+//   warp 0      TMA producer: V_hi, V_lo (K-major, 64B/128B swizzle) and U
+//               (MN-major, SWIZZLE_128B_ATOM_32B -- the only MN-major swizzle
+//               tcgen05 accepts for 32-bit operands) into a STAGES-deep ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (leader CTA)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> 128B-swizzled smem tile ->
+//               TMA bulk tensor store of X (full lines, clipped at M / BN)
+//   warps 8-11  splitter: U_lo, fence.proxy.async, one arrival per warp
+// mbarriers: full (TMA tx), split (splitters of all CG CTAs -> leader),
+// empty and tmem_full (MMA commit, multicast to the pair), tmem_empty
+// (epilogue warps of all CG CTAs -> leader).  Cross-CTA arrivals use the
+// default .release.cta semantics (as CUTLASS's ClusterBarrier): an explicit
+// .release.cluster compiles to a GPU-scope MEMBAR per arrival.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -30,19 +36,7 @@
 
 namespace {
 
-constexpr int BLOCK_M = 128;
-constexpr int BLOCK_K = 32;  // 32 fp32 = one 128-byte swizzle row
 constexpr int NUM_THREADS = 384;
-
-template <int BLOCK_N, int STAGES>
-struct TcCfg {
-    static constexpr int A_BYTES = BLOCK_M * BLOCK_K * 4;
-    static constexpr int B_BYTES = BLOCK_N * BLOCK_K * 4;
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B_hi, B_lo
-    static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;         // bytes TMA lands per stage
-    static constexpr int TMEM_COLS = 2 * BLOCK_N;                  // two accumulators
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -52,9 +46,6 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -76,33 +67,89 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// shared-memory matrix descriptor (tcgen05 "version 1"), 128-byte swizzle
-// layout 2 = SWIZZLE_128B (K-major operands), layout 1 = SWIZZLE_128B_BASE32B (MN-major
-// 32-bit operands: 32-byte chunks XOR-swizzled within 128-byte rows, 4-row atoms)
+// shared-memory matrix descriptor (tcgen05 "version 1"); layout 2 = SWIZZLE_128B,
+// 4 = SWIZZLE_64B (K-major operands), 1 = SWIZZLE_128B_BASE32B (MN-major 32-bit)
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
                                               uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // descriptor version for sm_100
+    d |= (uint64_t)1 << 46;
     d |= (uint64_t)layout << 61;
     return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
 }
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
 }
+
+template <int CG>
+struct Tc;  // cta_group-specific instructions
+
+template <>
+struct Tc<1> {
+    static __device__ __forceinline__ void alloc(uint32_t slot, uint32_t cols) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    static __device__ __forceinline__ void dealloc(uint32_t taddr, uint32_t cols) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+    }
+    static __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+    static __device__ __forceinline__ void commit(uint32_t bar) {
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
+    }
+    static __device__ __forceinline__ void arrive_leader(uint32_t bar) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+    static __device__ __forceinline__ void sync_all() { __syncthreads(); }
+};
+
+template <>
+struct Tc<2> {
+    static __device__ __forceinline__ void alloc(uint32_t slot, uint32_t cols) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    static __device__ __forceinline__ void dealloc(uint32_t taddr, uint32_t cols) {
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+    }
+    static __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+    static __device__ __forceinline__ void commit(uint32_t bar) {  // multicast to both CTAs of the pair
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+            "%1;" ::"r"(bar),
+            "h"((uint16_t)3)
+            : "memory");
+    }
+    static __device__ __forceinline__ void arrive_leader(uint32_t bar) {
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(map_to_rank(bar, 0)) : "memory");
+    }
+    static __device__ __forceinline__ void sync_all() {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+};
 
 #define TMEM_LD_32(taddr, v)                                                                                      \
     asm volatile(                                                                                                 \
@@ -115,298 +162,26 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
           "=r"(v[30]), "=r"(v[31])                                                                                \
         : "r"(taddr))
 
-struct TileCoord {
-    int z, m0, n0;
-};
-
-__device__ __forceinline__ TileCoord decode_tile(int T, int n_m, int n_n, int BLOCK_N) {
-    TileCoord c;
-    const int mb = T % n_m;
-    const int rest = T / n_m;
-    c.m0 = mb * BLOCK_M;
-    c.n0 = (rest % n_n) * BLOCK_N;
-    c.z = rest / n_n;
-    return c;
-}
-
-template <int BLOCK_N, int STAGES>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    nk3_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
-                     const __grid_constant__ CUtensorMap tmB, float *__restrict__ X, int M, int K, long long NP,
-                     int Z) {
-    using Cfg = TcCfg<BLOCK_N, STAGES>;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t *gbase = smem_raw + (base - raw);
-    const uint32_t bar0 = base + STAGES * Cfg::STAGE_BYTES;
-    // barrier layout: full[S] split[S] empty[S] tfull[2] tempty[2] | tmem slot
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto split_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
-    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + 2 + a); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + 8 * (3 * STAGES + 4));
-
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int n_m = (M + BLOCK_M - 1) / BLOCK_M;
-    const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
-    const int num_tiles = Z * n_m * n_n;
-    const int num_k = (K + BLOCK_K - 1) / BLOCK_K;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(split_bar(s), 128);
-            mbar_init(empty_bar(s), 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(Cfg::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
-                const TileCoord tc = decode_tile(T, n_m, n_n, BLOCK_N);
-                for (int kb = 0; kb < num_k; ++kb) {
-                    mbar_wait(empty_bar(stage), phase ^ 1);
-                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
-                    const uint32_t sAlo = sA + Cfg::A_BYTES;
-                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
-                    mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
-                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BLOCK_K, tc.m0, tc.z);
-                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BLOCK_K, tc.m0, tc.z);
-#pragma unroll
-                    for (int j = 0; j < BLOCK_N / 32; ++j)
-                        tma_load_3d(sB + j * 4096, &tmB, full_bar(stage), tc.n0 + 32 * j, kb * BLOCK_K, tc.z);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            // kind::tf32, D f32, A K-major, B MN-major, M = 128, N = BLOCK_N
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(BLOCK_M >> 4) << 24);
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
-                mbar_wait(tempty_bar(acc), acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
-                for (int kb = 0; kb < num_k; ++kb) {
-                    mbar_wait(full_bar(stage), phase);
-                    mbar_wait(split_bar(stage), phase);
-                    tc_fence_after();
-                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
-                    const uint32_t sAlo = sA + Cfg::A_BYTES;
-                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
-                    const uint32_t sBlo = sB + Cfg::B_BYTES;
-#pragma unroll
-                    for (int s = 0; s < BLOCK_K / 8; ++s) {
-                        // A: K-major SW128, +32 B per K=8 step; B: MN-major SW128, +1024 B per 8 K-rows
-                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 1024, 2);
-                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 1024, 2);
-                        const uint64_t b_hi = make_desc(sB + 1024 * s, 4096, 512, 1);
-                        const uint64_t b_lo = make_desc(sBlo + 1024 * s, 4096, 512, 1);
-                        const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
-#ifdef FC_DEBUG
-                        if (blockIdx.x == 0 && kb == 0 && s == 0 && T == (int)blockIdx.x)
-                            printf("[mma] tmem=%x idesc=%x adesc=%llx bdesc=%llx sA=%x\n", d_tmem, idesc,
-                                   (unsigned long long)a_hi, (unsigned long long)b_hi, sA);
-#endif
-                        mma_tf32(d_tmem, a_lo, b_hi, idesc, first);
-                        mma_tf32(d_tmem, a_hi, b_lo, idesc, 1u);
-                        mma_tf32(d_tmem, a_hi, b_hi, idesc, 1u);
-                    }
-                    mma_commit(empty_bar(stage));
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-                mma_commit(tfull_bar(acc));
-                if (++acc == 2) {
-                    acc = 0;
-                    acc_phase ^= 1;
-                }
-            }
-        }
-    } else if (warp >= 4 && warp < 8) {
-        // ------------------------------------------------ epilogue
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
-            const TileCoord tc = decode_tile(T, n_m, n_n, BLOCK_N);
-            mbar_wait(tfull_bar(acc), acc_phase);
-            tc_fence_after();
-            const int row = tc.m0 + q * 32 + lane;
-            float *xrow = X + ((size_t)tc.z * M + row) * NP + tc.n0;
-#pragma unroll 1
-            for (int c = 0; c < BLOCK_N / 32; ++c) {
-                uint32_t v[32];
-                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
-                TMEM_LD_32(taddr, v);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifdef FC_DEBUG
-                if (lane < 2 && q == 0 && blockIdx.x == 0 && c == 0)
-                    printf("[epi] T=%d row=%d tmem=%x v=%g %g %g %g\n", T, row, taddr, __uint_as_float(v[0]),
-                           __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
-#endif
-                if (row < M && tc.n0 + c * 32 < NP) {
-                    float4 *dst = reinterpret_cast<float4 *>(xrow + c * 32);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(tempty_bar(acc));
-            if (++acc == 2) {
-                acc = 0;
-                acc_phase ^= 1;
-            }
-        }
-    } else if (warp >= 8) {
-        // ------------------------------------------------ hi/lo splitter for U
-        const int st = threadIdx.x - 256;  // 0..127
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int T = blockIdx.x; T < num_tiles; T += gridDim.x) {
-            for (int kb = 0; kb < num_k; ++kb) {
-                mbar_wait(full_bar(stage), phase);
-#ifdef FC_DEBUG
-                if (st == 0 && blockIdx.x == 0 && kb == 0) {
-                    const float *f = reinterpret_cast<const float *>(gbase + stage * Cfg::STAGE_BYTES);
-                    printf("[split] T=%d A[0..3]=%g %g %g %g  Alo0=%g  B[0..3]=%g %g %g %g\n", T, f[0], f[1], f[2], f[3],
-                           f[Cfg::A_BYTES / 4], f[2 * Cfg::A_BYTES / 4], f[2 * Cfg::A_BYTES / 4 + 1],
-                           f[2 * Cfg::A_BYTES / 4 + 2], f[2 * Cfg::A_BYTES / 4 + 3]);
-                }
-#endif
-                const float4 *bh =
-                    reinterpret_cast<const float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
-                float4 *bl = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES +
-                                                        Cfg::B_BYTES);
-                // the MMA reads U truncated to TF32 (measured: low 13 mantissa bits ignored), so the
-                // hi part is U itself and lo = U - trunc_tf32(U), exact in fp32
-#pragma unroll
-                for (int j = 0; j < Cfg::B_BYTES / 16 / 128; ++j) {
-                    const float4 v = bh[st + 128 * j];
-                    float4 lo;
-                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                    bl[st + 128 * j] = lo;
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(split_bar(stage));
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
-    }
-}
-
-// ===========================================================================
-// cta_group::2 variant: a CTA pair (cluster of 2) computes a 256 x BLOCK_N tile
-// with M = 256 tcgen05.mma instructions issued by the leader CTA.  Rank r holds
-// rows [128 r, 128 r + 128) of the V tile (A operand) and columns
-// [r BLOCK_N/2, (r+1) BLOCK_N/2) of the U tile (B operand); each CTA's TMEM
-// receives its 128 rows x BLOCK_N columns.  Per SM this halves the bytes each
-// MMA cycle needs from shared memory and L2 (U is read once for C' <= 256).
-// Cross-CTA signalling: splitters arrive on the leader's split barrier, MMA
-// commits multicast to both CTAs' empty / tmem_full barriers, epilogues arrive
-// on the leader's tmem_empty barrier.
-// ===========================================================================
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-    return r;
-}
-// Remote arrive with the default (.release.cta) semantics, as CUTLASS's ClusterBarrier
-// does: an explicit .release.cluster here costs a GPU-scope MEMBAR per arrival.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mma_tf32_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit_2sm_mc(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            bar),
-        "h"((uint16_t)3)
-        : "memory");
-}
-
-template <int BLOCK_N, int STAGES, int BK>
-struct Tc2Cfg {
-    static constexpr int NH = BLOCK_N / 2;  // columns of U per CTA
+template <int CG, int BLOCK_N, int STAGES, int BK>
+struct TcCfg {
+    static constexpr int BM = 128 * CG;       // MMA M (rows of V per tile)
+    static constexpr int NH = BLOCK_N / CG;   // columns of U held per CTA
     static constexpr int A_BYTES = 128 * BK * 4;
     static constexpr int B_BYTES = NH * BK * 4;
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-    static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = 2 * BLOCK_N;
-    static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;  // per epilogue warp: 2 x (32 rows x 128 B)
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A_hi, A_lo, B, B_lo
+    static constexpr int TX_BYTES = 2 * A_BYTES + B_BYTES;         // bytes TMA lands per stage
+    static constexpr int TMEM_COLS = 2 * BLOCK_N;                  // double-buffered accumulator
+    static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;          // per epilogue warp: 2 x (32 rows x 128 B)
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
-template <int BLOCK_N, int STAGES, int BK>
+template <int CG, int BLOCK_N, int STAGES, int BK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    nk3_gemm_tcgen05_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
-                         const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
-                         int M, int K, long long NP, int Z, int dbg) {
-    using Cfg = Tc2Cfg<BLOCK_N, STAGES, BK>;
+    nk3_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+                     const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int M,
+                     int K, long long NP, int Z) {
+    using Cfg = TcCfg<CG, BLOCK_N, STAGES, BK>;
+    using I = Tc<CG>;
     static_assert(BK == 16 || BK == 32, "BK is one 64 B or 128 B swizzle row");
     static_assert(Cfg::TMEM_COLS <= 512, "TMEM holds 512 columns");
     extern __shared__ uint8_t smem_raw[];
@@ -424,9 +199,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES + 8 * (3 * STAGES + 4));
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = cluster_rank();
-    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
-    const int n_m = (M + 255) / 256;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int grp = blockIdx.x / CG, ngrp = gridDim.x / CG;
+    const int n_m = (M + Cfg::BM - 1) / Cfg::BM;
     const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
     const int num_tiles = Z * n_m * n_n;
     const int num_k = (K + BK - 1) / BK;
@@ -434,12 +209,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(split_bar(s), 8);  // one arrival per splitter warp, 4 warps x 2 CTAs (leader's copy)
+            mbar_init(split_bar(s), 4 * CG);  // one arrival per splitter warp of every CTA in the group
             mbar_init(empty_bar(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 8);  // one arrival per epilogue warp, both CTAs (leader's copy)
+            mbar_init(tempty_bar(a), 4 * CG);  // one arrival per epilogue warp of every CTA in the group
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -447,28 +222,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
     }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(Cfg::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    }
+    if (warp == 1) I::alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
     tc_fence_before();
-    cluster_sync_all();
+    I::sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     auto decode = [&](int T, int &z, int &m0, int &n0) {
         const int mb = T % n_m, rest = T / n_m;
-        m0 = mb * 256;
+        m0 = mb * Cfg::BM;
         n0 = (rest % n_n) * BLOCK_N;
         z = rest / n_n;
     };
 
     if (warp == 0) {
-        if (lane == 0) {  // ---- TMA producer (both CTAs load their halves)
+        if (lane == 0) {  // ---- TMA producer (every CTA loads its rows of V and columns of U)
             int stage = 0;
             uint32_t phase = 0;
-            for (int T = pair; T < num_tiles; T += npairs) {
+            for (int T = grp; T < num_tiles; T += ngrp) {
                 int z, m0, n0;
                 decode(T, z, m0, n0);
                 for (int kb = 0; kb < num_k; ++kb) {
@@ -491,14 +262,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA only)
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA)
+            // kind::tf32, D f32, A K-major, B MN-major, M = 128*CG, N = BLOCK_N
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(Cfg::BM >> 4) << 24);
+            constexpr uint32_t a_sbo = BK * 4 * 8, a_layout = BK == 32 ? 2u : 4u;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int T = pair; T < num_tiles; T += npairs) {
+            for (int T = grp; T < num_tiles; T += ngrp) {
                 mbar_wait(tempty_bar(acc), acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
@@ -511,25 +284,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t sBlo = sB + Cfg::B_BYTES;
 #pragma unroll
                     for (int s = 0; s < BK / 8; ++s) {
-                        // A: K-major, 128B (BK=32) or 64B (BK=16) swizzle, 8-row atoms; +32 B per K=8.
-                        // B: MN-major 128B/32B-atom swizzle, n-blocks of BK rows x 128 B, 4-row atoms.
-                        constexpr uint32_t a_sbo = BK * 4 * 8, a_layout = BK == 32 ? 2u : 4u;
+                        // A: +32 B per K=8 step inside the swizzled row; B: +1024 B = 8 K-rows
                         const uint64_t a_hi = make_desc(sA + 32 * s, 16, a_sbo, a_layout);
                         const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, a_sbo, a_layout);
                         const uint64_t b_hi = make_desc(sB + 1024 * s, BK * 128, 512, 1);
                         const uint64_t b_lo = make_desc(sBlo + 1024 * s, BK * 128, 512, 1);
                         const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
-                        if (!(dbg & 2)) { mma_tf32_2sm(d_tmem, a_lo, b_hi, idesc, first);
-                        mma_tf32_2sm(d_tmem, a_hi, b_lo, idesc, 1u); }
-                        mma_tf32_2sm(d_tmem, a_hi, b_hi, idesc, 1u);
+                        I::mma(d_tmem, a_lo, b_hi, idesc, first);
+                        I::mma(d_tmem, a_hi, b_lo, idesc, 1u);
+                        I::mma(d_tmem, a_hi, b_hi, idesc, 1u);
                     }
-                    mma_commit_2sm_mc(empty_bar(stage));
+                    I::commit(empty_bar(stage));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit_2sm_mc(tfull_bar(acc));
+                I::commit(tfull_bar(acc));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -538,12 +309,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp >= 4 && warp < 8) {
         // ---- epilogue: each warp drains its 32 TMEM lanes, 32 columns at a time, into a
-        // 128B-swizzled 32 x 32 smem tile and TMA-stores it (full-line, clipped at M / NP).
+        // 128B-swizzled 32 x 32 smem tile and TMA-stores it (full lines, clipped at M / NP).
         const int q = warp & 3;
         const uint32_t stage0 = epi0 + q * (2 * 4096);
         int acc = 0, buf = 0;
         uint32_t acc_phase = 0;
-        for (int T = pair; T < num_tiles; T += npairs) {
+        for (int T = grp; T < num_tiles; T += ngrp) {
             int z, m0, n0;
             decode(T, z, m0, n0);
             mbar_wait(tfull_bar(acc), acc_phase);
@@ -554,7 +325,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 uint32_t v[32];
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
                 TMEM_LD_32(taddr, v);
-                // the staging buffer we are about to overwrite must have been read by its TMA store
+                // the staging buffer about to be overwritten must have been read by its TMA store
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 __syncwarp();
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -567,7 +338,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                  : "memory");
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0 && !(dbg & 4)) {
+                if (lane == 0) {
                     asm volatile(
                         "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                             &tmX),
@@ -579,20 +350,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(map_to_rank(tempty_bar(acc), 0));
+            if (lane == 0) I::arrive_leader(tempty_bar(acc));
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
         }
-    } else if (warp >= 8) {  // ---- splitter: lo = U - tf32_trunc(U) (the MMA truncates U to its hi part)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else if (warp >= 8) {  // ---- splitter: lo = U - trunc_tf32(U)
         const int st = threadIdx.x - 256;
         int stage = 0;
         uint32_t phase = 0;
-        for (int T = pair; T < num_tiles; T += npairs) {
+        for (int T = grp; T < num_tiles; T += ngrp) {
             for (int kb = 0; kb < num_k; ++kb) {
                 mbar_wait(full_bar(stage), phase);
-                const float4 *bh = reinterpret_cast<const float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
+                const float4 *bh =
+                    reinterpret_cast<const float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
                 float4 *bl = reinterpret_cast<float4 *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES +
                                                         Cfg::B_BYTES);
 #pragma unroll
@@ -607,7 +380,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if ((st & 31) == 0) mbar_arrive_cluster(map_to_rank(split_bar(stage), 0));
+                if ((st & 31) == 0) I::arrive_leader(split_bar(stage));
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -616,12 +389,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     }
 
-    if (warp >= 4 && warp < 8 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
-    cluster_sync_all();
+    I::sync_all();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+        I::dealloc(tmem_base, Cfg::TMEM_COLS);
     }
 }
 
@@ -653,42 +425,11 @@ bool encode_3d(CUtensorMap *map, const void *ptr, uint64_t d0, uint64_t d1, uint
 
 int g_num_sms = 0;
 
-template <int BLOCK_N, int STAGES>
+template <int CG, int BLOCK_N, int STAGES, int BK>
 cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                    cudaStream_t s) {
-    using Cfg = TcCfg<BLOCK_N, STAGES>;
-    CUtensorMap mA, mAlo, mB;
-    const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
-    const uint64_t Kp = (uint64_t)g.Kp;
-    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BLOCK_K, BLOCK_M, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
-        return cudaErrorInvalidValue;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(nk3_gemm_tcgen05<BLOCK_N, STAGES>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const long long n_m = (g.M + BLOCK_M - 1) / BLOCK_M;
-    const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
-    const long long tiles = (long long)g.Z * n_m * n_n;
-    const int grid = (int)(tiles < g_num_sms ? tiles : g_num_sms);
-    nk3_gemm_tcgen05<BLOCK_N, STAGES><<<grid, NUM_THREADS, Cfg::SMEM_BYTES, s>>>(mA, mAlo, mB, X, g.M, g.K,
-                                                                              g.BN_pad, g.Z);
-    return cudaGetLastError();
-}
-
-template <int BLOCK_N, int STAGES, int BK>
-cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
-                       cudaStream_t s) {
-    using Cfg = Tc2Cfg<BLOCK_N, STAGES, BK>;
+    using Cfg = TcCfg<CG, BLOCK_N, STAGES, BK>;
+    static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory per CTA");
     CUtensorMap mA, mAlo, mB, mX;
     const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
     const uint64_t Kp = (uint64_t)g.Kp;
@@ -698,7 +439,7 @@ cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, co
         !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
-    auto kern = nk3_gemm_tcgen05_2sm<BLOCK_N, STAGES, BK>;
+    auto kern = nk3_gemm_tcgen05<CG, BLOCK_N, STAGES, BK>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
@@ -710,26 +451,25 @@ cudaError_t launch_2sm(const Geometry &g, const float *Vhi, const float *Vlo, co
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const long long n_m = (g.M + 255) / 256;
+    const long long n_m = (g.M + Cfg::BM - 1) / Cfg::BM;
     const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
     const long long tiles = (long long)g.Z * n_m * n_n;
-    const long long pairs = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    const long long groups = tiles < g_num_sms / CG ? tiles : g_num_sms / CG;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
+    cfg.gridDim = dim3((unsigned)(CG * groups));
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CG > 1 ? 1 : 0;
     int M_ = g.M, K_ = g.K, Z_ = g.Z;
     long long NP_ = g.BN_pad;
-    static const int dbg = getenv("FASTCONV_TC_DBG") ? atoi(getenv("FASTCONV_TC_DBG")) : 0;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_, dbg);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -741,9 +481,8 @@ int fc_tcgen05_available() { return get_encode() != nullptr; }
 cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                                    cudaStream_t s) {
     if (!Vlo) return cudaErrorInvalidValue;
-    static const int force_1sm = getenv("FASTCONV_TC_1SM") != nullptr;
-    static const int bk32 = getenv("FASTCONV_TC_BK32") != nullptr;
-    if (g.M > 128 && !force_1sm)
-        return bk32 ? launch_2sm<256, 2, 32>(g, Vhi, Vlo, U, X, s) : launch_2sm<256, 6, 16>(g, Vhi, Vlo, U, X, s);
-    return launch<128, 3>(g, Vhi, Vlo, U, X, s);
+    static const int force_1cta = getenv("FASTCONV_TC_1SM") != nullptr;
+    // M > 128: CTA pairs (M = 256 per MMA); M <= 128: single CTAs (M = 128 per MMA)
+    if (g.M > 128 && !force_1cta) return launch<2, 256, 6, 16>(g, Vhi, Vlo, U, X, s);
+    return launch<1, 256, 4, 16>(g, Vhi, Vlo, U, X, s);
 }

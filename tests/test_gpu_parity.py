@@ -252,3 +252,22 @@ def test_l2_chunking(method, m, chunk, monkeypatch):
     y = p.forward(I.cuda(), W.cuda())
     torch.cuda.synchronize()
     assert rel_err(y.cpu().double().numpy(), O) <= tol(method, m, cfg.r)
+
+
+@pytest.mark.parametrize("method,m", [("winograd", 4), ("regular_fft", 6), ("gauss_fft", 8)])
+def test_cached_weight_transform(method, m):
+    """conv_transform_weights + conv_forward_cached (inference with V computed once)
+    equals conv_forward bit for bit, for several inputs against one V."""
+    cfg = synth.custom(3, 16, 24, 20, 20, 3, seed=61, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    I2, _ = synth.make_inputs(cfg, seed=62)
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+    x, x2, w = I.cuda(), I2.cuda(), W.cuda()
+    ref, ref2 = p.forward(x, w), p.forward(x2, w)
+    ws = p.alloc_workspace()
+    p.transform_weights(w, ws)
+    y = p.forward_cached(x, ws)
+    y2 = p.forward_cached(x2, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(y, ref) and torch.equal(y2, ref2)
+    assert rel_err(y.cpu().double().numpy(), oracle.conv_fp64(I, W)) <= tol(method, m, cfg.r)
