@@ -493,7 +493,8 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         auto smem_of = [&](int ipc, int r) {
             return (size_t)ipc * r * g.n_w * Sm * sizeof(float2) + (size_t)ipc * r * g.m * SWo * sizeof(float);
         };
-        const int target = 512 / H > 1 ? 512 / H : 1;
+        static const int items_env = getenv("FASTCONV_NK4F_ITEMS") ? atoi(getenv("FASTCONV_NK4F_ITEMS")) : 256;
+        const int target = items_env / H > 1 ? items_env / H : 1;
         int R = target / g.n_w > 0 ? target / g.n_w : 1, IPC = 1;
         if (R >= g.n_h) {
             R = g.n_h;
