@@ -289,6 +289,86 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
     }
 }
 
+// ---------------------------------------------------------------- FFT NK1 ---
+// One thread per (c', c) kernel, V = conj(DFT2(pad_t(g))) / t^2 with the
+// zero-padded r x r kernel (only r rows / columns contribute),
+// unrolled for compile-time (t, r) with constant-memory twiddles; the real
+// embedding (Regular) or the Gauss pre-sums and the 3xTF32 split are written
+// along c (coalesced).
+template <int T, int R>
+__global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restrict__ w, float *__restrict__ V,
+                                               float *__restrict__ Vlo, int split) {
+    constexpr int H = T / 2 + 1;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)g.C * g.Cout) return;
+    const int co = (int)(idx / g.C), c = (int)(idx - (long long)co * g.C);
+    const float *ker = w + idx * (R * R);
+    float k[R][R];
+#pragma unroll
+    for (int p = 0; p < R; ++p)
+#pragma unroll
+        for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
+    const float inv = 1.0f / ((float)T * (float)T);
+    const size_t zstride = (size_t)g.M * g.Kp;
+    auto put = [&](int z, int row, int col, float v) {
+        const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
+        if (split) {
+            uint32_t r;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+            const float hi = __uint_as_float(r);
+            V[o] = hi;
+            Vlo[o] = v - hi;
+        } else {
+            V[o] = v;
+        }
+    };
+#pragma unroll 1
+    for (int l = 0; l < H; ++l) {
+        cf tr[R];  // row DFT along q: sum_q g[p][q] W^{-l q}
+#pragma unroll
+        for (int p = 0; p < R; ++p) {
+            float ar = k[p][0], ai = 0.f;
+#pragma unroll
+            for (int q = 1; q < R; ++q) {
+                const int j = (l * q) % T;
+                const float2 tw = fct::c_tw[fct::tw_base(T) + j];
+                ar = fmaf(k[p][q], tw.x, ar);
+                ai = fmaf(-k[p][q], tw.y, ai);
+            }
+            tr[p] = cf{ar, ai};
+        }
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) {
+            cf acc = tr[0];
+#pragma unroll
+            for (int p = 1; p < R; ++p) {
+                const cf t = fct::twiddle_mul<T, -1>(tr[p], kk * p);
+                acc.x += t.x;
+                acc.y += t.y;
+            }
+            const float vr = acc.x * inv, vi = -acc.y * inv;  // conj(DFT) / t^2
+            const int e = kk * H + l;
+            if (g.method == CONV_REGULAR_FFT) {
+                put(e, co, c, vr);
+                put(e, co, g.C + c, -vi);
+                put(e, g.Cout + co, c, vi);
+                put(e, g.Cout + co, g.C + c, vr);
+            } else {  // Gauss: V_r, V_i - V_r, V_r + V_i
+                put(e, co, c, vr);
+                put(g.E + e, co, c, vi - vr);
+                put(2 * g.E + e, co, c, vr + vi);
+            }
+        }
+    }
+}
+
+template <int T, int R>
+cudaError_t launch_nk1_fft(const Geometry &g, const float *w, float *V, float *Vlo, int split, cudaStream_t s) {
+    const long long n = (long long)g.C * g.Cout;
+    nk1_fft<T, R><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, w, V, Vlo, split);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- FFT NK2 ---
 constexpr int FTN = 32;  // tiles per CTA
 
@@ -626,6 +706,22 @@ cudaError_t fc_launch_kernel_transform_fast(const Geometry &g, const ConvConsts 
         if (g.t == 6 && g.r == 3) return launch_nk1_wino<6, 3>(g, hc, w, V, Vlo, split, s);
         if (g.t == 8 && g.r == 3) return launch_nk1_wino<8, 3>(g, hc, w, V, Vlo, split, s);
         if (g.t == 6 && g.r == 5) return launch_nk1_wino<6, 5>(g, hc, w, V, Vlo, split, s);
+    } else if (g.r == 3) {
+        switch (g.t) {
+            case 8: return launch_nk1_fft<8, 3>(g, w, V, Vlo, split, s);
+            case 9: return launch_nk1_fft<9, 3>(g, w, V, Vlo, split, s);
+            case 10: return launch_nk1_fft<10, 3>(g, w, V, Vlo, split, s);
+            case 16: return launch_nk1_fft<16, 3>(g, w, V, Vlo, split, s);
+            case 24: return launch_nk1_fft<24, 3>(g, w, V, Vlo, split, s);
+            case 27: return launch_nk1_fft<27, 3>(g, w, V, Vlo, split, s);
+            case 32: return launch_nk1_fft<32, 3>(g, w, V, Vlo, split, s);
+        }
+    } else if (g.r == 5) {
+        switch (g.t) {
+            case 13: return launch_nk1_fft<13, 5>(g, w, V, Vlo, split, s);
+            case 18: return launch_nk1_fft<18, 5>(g, w, V, Vlo, split, s);
+            case 31: return launch_nk1_fft<31, 5>(g, w, V, Vlo, split, s);
+        }
     }
     *handled = 0;
     return cudaSuccess;
