@@ -262,6 +262,12 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
             G.Z = G.E; G.M = Cout; G.K = C;
         }
         G.Kp = (G.K + 3) / 4 * 4;
+        G.cplx = 0;
+        if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % 16 == 0 &&
+            !getenv("FASTCONV_NO_CPLX")) {
+            G.cplx = 1;
+            G.Kp = (C + 3) / 4 * 4;
+        }
     }
     *g = G;
     if (info) {
@@ -276,7 +282,7 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         I.nchunks = 1;
         if (method != CONV_DIRECT) {
             const int split = (gemm != CONV_GEMM_FFMA);
-            const size_t vb = (size_t)G.Z * G.M * G.Kp * 4;  // V_hi, then V_lo at the next 256 B boundary
+            const size_t vb = fc_v_floats(G) * 4;  // V_hi, then V_lo at the next 256 B boundary
             I.bytes_V = split ? align256(vb) + vb : vb;
             I.chunk = pick_chunk(G, I.bytes_V);
             I.nchunks = (B + I.chunk - 1) / I.chunk;
@@ -402,7 +408,7 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
             return CONV_ERR_CUDA;
         }
         p->off_V = 0;
-        const size_t vb = (size_t)g.Z * g.M * g.Kp * 4;
+        const size_t vb = fc_v_floats(g) * 4;
         p->off_Vlo = align256(vb);
         const size_t vtot = align256(p->info.bytes_V);
         p->off_U = vtot;

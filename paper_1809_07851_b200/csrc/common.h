@@ -30,6 +30,9 @@ struct Geometry {
     long long BN, BN_pad;
     int Z, M, K;  // contraction batch / rows (output channels side) / reduction
     int Kp;       // row pitch of V (K rounded up to 4 floats = 16 B, for TMA)
+    int cplx;     // Regular-FFT complex mode (tcgen05, C' % 256 == 0, C % 16 == 0): V stored as
+                  // (V_r, V_i) planes [E][2][C'][Kp], Kp = round4(C), instead of the 4x real
+                  // embedding; the contraction picks the plane per K-half and negates -V_i
 };
 
 struct conv_plan_s {
@@ -44,6 +47,11 @@ struct conv_plan_s {
     int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
     conv_plan_info info;
 };
+
+// floats of V (one of V_hi / V_lo)
+inline size_t fc_v_floats(const Geometry &g) {
+    return g.cplx ? (size_t)2 * g.E * g.Cout * g.Kp : (size_t)g.Z * g.M * g.Kp;
+}
 
 // geometry of a chunk of Bc images (U / X row pitch BN_pad follows the chunk)
 Geometry fc_chunk_geometry(const Geometry &g, int Bc);

@@ -179,7 +179,7 @@ template <int CG, int BLOCK_N, int STAGES, int BK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     nk3_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                      const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int M,
-                     int K, long long NP, int Z) {
+                     int K, long long NP, int Z, int cplx, int Mh, int kb_half) {
     using Cfg = TcCfg<CG, BLOCK_N, STAGES, BK>;
     using I = Tc<CG>;
     static_assert(BK == 16 || BK == 32, "BK is one 64 B or 128 B swizzle row");
@@ -248,8 +248,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint32_t sAlo = sA + Cfg::A_BYTES;
                     const uint32_t sB = sA + 2 * Cfg::A_BYTES;
                     mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
-                    tma_load_3d(sA, &tmA, full_bar(stage), kb * BK, m0 + 128 * (int)rank, z);
-                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), kb * BK, m0 + 128 * (int)rank, z);
+                    int ak = kb * BK, ar = m0 + 128 * (int)rank, az = z;
+                    if (cplx) {  // Re rows: [V_r | -V_i], Im rows: [V_i | V_r] over K = [U_r; U_i]
+                        const int re = m0 < Mh, hi = kb >= kb_half;
+                        ak = (kb - hi * kb_half) * BK;
+                        ar -= re ? 0 : Mh;
+                        az = 2 * z + (re ? hi : 1 - hi);
+                    }
+                    tma_load_3d(sA, &tmA, full_bar(stage), ak, ar, az);
+                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), ak, ar, az);
 #pragma unroll
                     for (int j = 0; j < Cfg::NH / 32; ++j)
                         tma_load_3d(sB + j * (BK * 128), &tmB, full_bar(stage), n0 + (int)rank * Cfg::NH + 32 * j,
@@ -264,8 +271,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA)
             // kind::tf32, D f32, A K-major, B MN-major, M = 128*CG, N = BLOCK_N
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
-                                   ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(Cfg::BM >> 4) << 24);
+            const uint32_t idesc0 = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                                    ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(Cfg::BM >> 4) << 24);
             constexpr uint32_t a_sbo = BK * 4 * 8, a_layout = BK == 32 ? 2u : 4u;
             int stage = 0;
             uint32_t phase = 0;
@@ -275,9 +282,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(tempty_bar(acc), acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+                const bool re_tile = cplx && (T % n_m) * Cfg::BM < Mh;
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(split_bar(stage), phase);
                     tc_fence_after();
+                    // complex mode: the Re rows' second K half multiplies -V_i (A negate bit)
+                    const uint32_t idesc = (re_tile && kb >= kb_half) ? (idesc0 | (1u << 13)) : idesc0;
                     const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
                     const uint32_t sAlo = sA + Cfg::A_BYTES;
                     const uint32_t sB = sA + 2 * Cfg::A_BYTES;
@@ -434,8 +444,11 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
     const uint64_t Kp = (uint64_t)g.Kp;
     const CUtensorMapSwizzle aswz = BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-    if (!encode_3d(&mA, Vhi, K, M, Z, Kp * 4, M * Kp * 4, BK, 128, aswz) ||
-        !encode_3d(&mAlo, Vlo, K, M, Z, Kp * 4, M * Kp * 4, BK, 128, aswz) ||
+    // V: [Z][M][Kp], or in complex mode the (V_r, V_i) planes [E][2][C'][Kp] with K = C
+    const uint64_t vK = g.cplx ? (uint64_t)g.C : K, vM = g.cplx ? (uint64_t)g.Cout : M;
+    const uint64_t vZ = g.cplx ? 2 * (uint64_t)g.E : Z;
+    if (!encode_3d(&mA, Vhi, vK, vM, vZ, Kp * 4, vM * Kp * 4, BK, 128, aswz) ||
+        !encode_3d(&mAlo, Vlo, vK, vM, vZ, Kp * 4, vM * Kp * 4, BK, 128, aswz) ||
         !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
@@ -469,7 +482,9 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     cfg.numAttrs = CG > 1 ? 1 : 0;
     int M_ = g.M, K_ = g.K, Z_ = g.Z;
     long long NP_ = g.BN_pad;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_);
+    int cplx_ = g.cplx, Mh_ = g.Cout, kbh_ = (g.C + BK - 1) / BK;
+    if (g.cplx && (g.Cout % Cfg::BM != 0 || g.C % BK != 0)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
     if (idx >= (long long)g.C * g.Cout) return;
     const int co = (int)(idx / g.C), c = (int)(idx % g.C);
     const float *ker = w + idx * r * r;
-    const size_t zstride = (size_t)g.M * g.Kp;
+    const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
     auto store = [&](int z, int row, int col, float v) {
         const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
         if (split) {
@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
             }
             const float vr = ar * inv, vi = -ai * inv;  // conj(DFT) / t^2
             const int e = k * h + l;
-            if (g.method == CONV_REGULAR_FFT) {
+            if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
+                store(2 * e, co, c, vr);
+                store(2 * e + 1, co, c, vi);
+            } else if (g.method == CONV_REGULAR_FFT) {  // real embedding [[V_r, -V_i], [V_i, V_r]]
                 store(e, co, c, vr);
                 store(e, co, g.C + c, -vi);
                 store(e, g.Cout + co, c, vi);

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
 #pragma unroll
         for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
     const float inv = 1.0f / ((float)T * (float)T);
-    const size_t zstride = (size_t)g.M * g.Kp;
+    const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
     auto put = [&](int z, int row, int col, float v) {
         const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
         if (split) {
@@ -348,7 +348,10 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
             }
             const float vr = acc.x * inv, vi = -acc.y * inv;  // conj(DFT) / t^2
             const int e = kk * H + l;
-            if (g.method == CONV_REGULAR_FFT) {
+            if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
+                put(2 * e, co, c, vr);
+                put(2 * e + 1, co, c, vi);
+            } else if (g.method == CONV_REGULAR_FFT) {  // real embedding [[V_r, -V_i], [V_i, V_r]]
                 put(e, co, c, vr);
                 put(e, co, g.C + c, -vi);
                 put(e, g.Cout + co, c, vi);

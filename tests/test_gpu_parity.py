@@ -271,3 +271,21 @@ def test_cached_weight_transform(method, m):
     torch.cuda.synchronize()
     assert torch.equal(y, ref) and torch.equal(y2, ref2)
     assert rel_err(y.cpu().double().numpy(), oracle.conv_fp64(I, W)) <= tol(method, m, cfg.r)
+
+
+def test_regular_complex_mode_matches_embedding(monkeypatch):
+    """Regular-FFT complex mode ((V_r, V_i) planes, A-negate for -V_i) gives exactly the
+    real-embedding result ([[V_r, -V_i], [V_i, V_r]] stored), and both match the oracle."""
+    cfg = synth.custom(2, 48, 256, 18, 18, 3, seed=71, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    x, w = I.cuda(), W.cuda()
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6)
+    y = p.forward(x, w)
+    monkeypatch.setenv("FASTCONV_NO_CPLX", "1")
+    pe = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6)
+    ye = pe.forward(x, w)
+    torch.cuda.synchronize()
+    assert p.info["bytes_V"] < pe.info["bytes_V"]  # half the V bytes
+    assert torch.equal(y, ye)
+    assert rel_err(y.cpu().double().numpy(), O) <= 1e-5
