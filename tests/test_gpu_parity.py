@@ -289,3 +289,14 @@ def test_regular_complex_mode_matches_embedding(monkeypatch):
     assert p.info["bytes_V"] < pe.info["bytes_V"]  # half the V bytes
     assert torch.equal(y, ye)
     assert rel_err(y.cpu().double().numpy(), O) <= 1e-5
+
+
+def test_accuracy_orderings():
+    """The paper's accuracy claims as orderings:
+    Winograd error grows with the tile t, the FFT error is flat in t and below Winograd's."""
+    I, W, O = _reduced("vgg3_2")
+    ew = {m: rel_err(run_gpu(I, W, "winograd", m), O) for m in (2, 4, 6)}
+    ef = {m: rel_err(run_gpu(I, W, "regular_fft", m), O) for m in (8, 14, 22, 30)}
+    assert ew[2] < ew[4] < ew[6]
+    assert max(ef.values()) <= 10 * min(ef.values())
+    assert ef[14] <= ew[6]
