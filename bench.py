@@ -365,7 +365,7 @@ def main():
         e2e_ms = parallel.max_over_ranks(s0.elapsed_time(s1) / args.e2e_steps, dev)
         e2e = {"value": cfg.direct_flops * world / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": I.numel() * 4 + W.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
-               "api": "conv_forward_host (pinned host in/w/out, H2D + 4 stage kernels + D2H per step)"}
+               "api": "conv_forward_host (pinned host in/w/out; H2D, kernels and D2H pipelined over 8 image chunks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -126,9 +126,12 @@ conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w
                                   void *workspace, size_t workspace_bytes, void *stream,
                                   float stage_ms[4]);
 
-/* End-to-end call with HOST buffers: copies h_in, h_w (ideally pinned) to the
- * caller-provided device buffers d_in, d_w, runs conv_forward, copies d_out
- * back to h_out, all asynchronously on `stream` (the caller synchronises). */
+/* End-to-end call with HOST buffers: copies h_in, h_w (pinned for overlap) to the
+ * caller-provided device buffers d_in, d_w, runs the forward pass, copies d_out
+ * back to h_out.  The batch is pipelined in image chunks (FASTCONV_E2E_CHUNKS,
+ * default 8): H2D of chunk i+1, the kernels of chunk i and D2H of chunk i-1
+ * overlap on plan-owned copy streams.  Asynchronous: when `stream` (the
+ * caller's) completes, h_out holds the result (the caller synchronises). */
 conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w, float *h_out,
                               float *d_in, float *d_w, float *d_out,
                               void *workspace, size_t workspace_bytes, void *stream);

@@ -418,6 +418,19 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
     }
     p->chunk = p->info.chunk;
     p->nchunks = p->info.nchunks;
+    {
+        const char *ev = getenv("FASTCONV_E2E_CHUNKS");
+        p->e2e_chunks = ev ? atoi(ev) : 8;
+        if (p->e2e_chunks < 1) p->e2e_chunks = 1;
+    }
+    if (method != CONV_DIRECT && p->e2e_chunks > 1) {  // copy streams for the pipelined host path
+        if (cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            if (p->h2d) cudaStreamDestroy(p->h2d);
+            p->h2d = p->d2h = nullptr;  // falls back to the serial host path
+        }
+    }
     *out = p;
     return CONV_OK;
 }
@@ -429,11 +442,13 @@ conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, in
 
 void conv_destroy(conv_plan_t p) {
     if (!p) return;
-    if (p->d_consts) {
+    if (p->d_consts || p->h2d || p->d2h) {
         int cur = -1;
         cudaGetDevice(&cur);
         if (cur != p->device) cudaSetDevice(p->device);
-        cudaFree(p->d_consts);
+        if (p->d_consts) cudaFree(p->d_consts);
+        if (p->h2d) cudaStreamDestroy(p->h2d);
+        if (p->d2h) cudaStreamDestroy(p->d2h);
         if (cur >= 0 && cur != p->device) cudaSetDevice(cur);
     }
     free(p);
@@ -800,14 +815,68 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
     if (st) return st;
     const Geometry &g = p->g;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t nin = (size_t)g.B * g.C * g.H * g.W * 4, nw = (size_t)g.Cout * g.C * g.r * g.r * 4;
-    const size_t nout = (size_t)g.B * g.Cout * g.Ho * g.Wo * 4;
-    cudaError_t e = cudaMemcpyAsync(d_in, h_in, nin, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_w, h_w, nw, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return launch_result(e, "H2D copy");
-    st = conv_forward(p, d_in, d_w, d_out, ws, ws_bytes, stream);
+    const size_t img_in = (size_t)g.C * g.H * g.W, img_out = (size_t)g.Cout * g.Ho * g.Wo;
+    const size_t nw = (size_t)g.Cout * g.C * g.r * g.r * 4;
+    cudaError_t e = cudaMemcpyAsync(d_w, h_w, nw, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return launch_result(e, "H2D copy (weights)");
+    if (g.method == CONV_DIRECT || !p->h2d || !p->d2h) {
+        e = cudaMemcpyAsync(d_in, h_in, img_in * g.B * 4, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return launch_result(e, "H2D copy");
+        if ((st = forward_impl(p, d_in, d_w, d_out, (char *)ws, s, nullptr))) return st;
+        return launch_result(cudaMemcpyAsync(h_out, d_out, img_out * g.B * 4, cudaMemcpyDeviceToHost, s),
+                             "D2H copy");
+    }
+    // Pipelined over image chunks: the H2D of chunk i+1 (copy stream), the kernels of
+    // chunk i (caller's stream) and the D2H of chunk i-1 (second copy stream) overlap;
+    // PCIe runs both directions at once.  The plan's own chunk (<= this one) sizes U / X.
+    const int nck = p->e2e_chunks < g.B ? p->e2e_chunks : g.B;
+    const int per = (g.B + nck - 1) / nck;
+    std::vector<cudaEvent_t> evs;
+    auto mk = [&]() -> cudaEvent_t {
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) evs.push_back(ev);
+        return ev;
+    };
+    cudaEvent_t start = mk();
+    e = cudaEventRecord(start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h2d, start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->d2h, start, 0);
+    if (e == cudaSuccess && (st = run_stage(p, g, 0, nullptr, d_w, nullptr, (char *)ws, s))) {
+        for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+        return st;
+    }
+    for (int b0 = 0; b0 < g.B && e == cudaSuccess && !st; b0 += per) {
+        const int nb = g.B - b0 < per ? g.B - b0 : per;
+        cudaEvent_t in_ready = mk(), out_ready = mk();
+        if (!in_ready || !out_ready) {
+            e = cudaErrorMemoryAllocation;
+            break;
+        }
+        e = cudaMemcpyAsync(d_in + (size_t)b0 * img_in, h_in + (size_t)b0 * img_in, (size_t)nb * img_in * 4,
+                            cudaMemcpyHostToDevice, p->h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(in_ready, p->h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, in_ready, 0);
+        if (e != cudaSuccess) break;
+        for (int c0 = 0; c0 < nb && !st; c0 += p->chunk) {
+            const int bc = nb - c0 < p->chunk ? nb - c0 : p->chunk;
+            const Geometry gc = fc_chunk_geometry(g, bc);
+            const float *in_c = d_in + (size_t)(b0 + c0) * img_in;
+            float *out_c = d_out + (size_t)(b0 + c0) * img_out;
+            for (int k = 1; k < 4 && !st; ++k) st = run_stage(p, gc, k, in_c, d_w, out_c, (char *)ws, s);
+        }
+        if (st) break;
+        e = cudaEventRecord(out_ready, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->d2h, out_ready, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out + (size_t)b0 * img_out, d_out + (size_t)b0 * img_out, (size_t)nb * img_out * 4,
+                                cudaMemcpyDeviceToHost, p->d2h);
+    }
+    cudaEvent_t done = mk();
+    if (e == cudaSuccess && done) e = cudaEventRecord(done, p->d2h);
+    if (e == cudaSuccess && done) e = cudaStreamWaitEvent(s, done, 0);  // caller's stream sees the D2H
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);                     // released once completed
     if (st) return st;
-    return launch_result(cudaMemcpyAsync(h_out, d_out, nout, cudaMemcpyDeviceToHost, s), "D2H copy");
+    return launch_result(e, "pipelined host forward");
 }
 
 }  // extern "C"

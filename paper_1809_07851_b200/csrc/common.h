@@ -45,6 +45,8 @@ struct conv_plan_s {
     int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
     int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
+    int e2e_chunks;                       // pipelining depth of conv_forward_host
+    cudaStream_t h2d, d2h;                // copy streams of the pipelined host path
     conv_plan_info info;
 };
 

@@ -300,3 +300,22 @@ def test_accuracy_orderings():
     assert ew[2] < ew[4] < ew[6]
     assert max(ef.values()) <= 10 * min(ef.values())
     assert ef[14] <= ew[6]
+
+
+@pytest.mark.parametrize("method,m", [("winograd", 4), ("gauss_fft", 6), ("direct", 0)])
+def test_forward_host_pipelined(method, m):
+    """conv_forward_host pipelines H2D / kernels / D2H over image chunks on plan-owned
+    copy streams; the host result equals the device-resident forward bit for bit."""
+    cfg = synth.custom(7, 12, 20, 21, 17, 3, seed=81, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+    ref = p.forward(I.cuda(), W.cuda())
+    hi, hw = I.pin_memory(), W.pin_memory()
+    ho = torch.full(p.out_shape, float("nan")).pin_memory()
+    di, dw = torch.empty_like(I, device="cuda"), torch.empty_like(W, device="cuda")
+    do = torch.empty(p.out_shape, device="cuda")
+    ws = p.alloc_workspace()
+    for _ in range(2):
+        p.forward_host(hi, hw, ho, di, dw, do, ws)
+    torch.cuda.current_stream().synchronize()
+    assert torch.equal(ho, ref.cpu())
