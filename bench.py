@@ -44,6 +44,16 @@ METRIC = "ms/layer & effective TFLOP/s (direct-conv FLOPs) + roofline fraction, 
 UNIT = "TFLOP/s"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 TF32_OVER_BF16 = 0.5  # nominal dense ratio (1.1 vs 2.25 PFLOP/s, B200_PROFILING.md)
+F16_OVER_BF16 = 1.0   # kind::f16 (fp16 in, fp32 accumulate) runs at the bf16 dense rate
+
+
+def contraction_peak(gemm: str, bf16_burst: float):
+    """fp32-equivalent TFLOP/s ceiling of NK3: three tensor-core products per fp32 product."""
+    if gemm == "tcgen05_f16x3":
+        return bf16_burst * F16_OVER_BF16 / 3.0, "bf16 burst x 1.0 (FP16/BF16 nominal) / 3 (F16X3 split)"
+    if gemm == "ffma":
+        return None, "FFMA (no tensor peak)"
+    return bf16_burst * TF32_OVER_BF16 / 3.0, "bf16 burst x 0.5 (TF32/BF16 nominal) / 3 (3xTF32 split)"
 
 
 def load_peaks():
@@ -179,7 +189,7 @@ def main():
     ap.add_argument("--workload", default="vgg3_2")
     ap.add_argument("--method", default="auto", help="auto (sweep) or winograd|regular_fft|gauss_fft|direct")
     ap.add_argument("--m", type=int, default=0)
-    ap.add_argument("--gemm", default="auto", choices=["auto", "tcgen05", "ffma"])
+    ap.add_argument("--gemm", default="auto", choices=["auto", "tcgen05", "ffma", "f16x3"])
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-baseline-s", type=float, default=12.0)
@@ -245,14 +255,16 @@ def main():
     method, m = best["method"], best["m"]
     # the paper's model (stage-sum roofline) against the measured sweep
     from paper_1809_07851_b200 import planner
+    plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
+    ws = plan.alloc_workspace(dev)
+    info = plan.info
+    gemm_name = fc.GEMM_NAMES.get(info["gemm"], args.gemm)
+    c_peak, c_peak_src = contraction_peak(gemm_name, bf16_burst)
     plan_report = planner.report(
         {(d["method"], d["m"]): fc.plan_query(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, d["method"], d["m"])
          for d in sweep.values() if d["method"] != "direct"},
         {(d["method"], d["m"]): d["ms"] for d in sweep.values()},
-        hbm_peak, tf32_peak / 3.0)
-    plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
-    ws = plan.alloc_workspace(dev)
-    info = plan.info
+        hbm_peak, c_peak or tf32_peak / 3.0)
     nst = 4 if method != "direct" else 1
 
     # ---- timed region -------------------------------------------------------------
@@ -289,13 +301,21 @@ def main():
     stages = []
     for s in range(nst):
         tsec = stage_ms[s] * 1e-3
-        if nst == 4 and s == 2:
-            flops = info["alg_flops"][2]
-            peak = tf32_peak / 3.0
-            ach = flops / tsec / 1e12
-            stages.append({"kernel": names[s], "ms": stage_ms[s], "bound": "tensor", "achieved": ach,
-                           "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                           "hbm_gbs": info["alg_bytes"][2] / tsec / 1e9})
+        if nst == 4 and s == 2 and c_peak:
+            # the binding roofline of the contraction: max(FLOPs / tensor ceiling, bytes / HBM)
+            flops, byts = info["alg_flops"][2], info["alg_bytes"][2]
+            t_tc, t_hbm = flops / (c_peak * 1e12), byts / (hbm_peak * 1e9)
+            tens = {"tensor_tflops": flops / tsec / 1e12, "tensor_peak": c_peak,
+                    "tensor_frac": flops / tsec / 1e12 / c_peak, "hbm_gbs": byts / tsec / 1e9,
+                    "hbm_frac": byts / tsec / 1e9 / hbm_peak}
+            if t_tc >= t_hbm:
+                stages.append(dict({"kernel": names[s], "ms": stage_ms[s], "bound": "tensor",
+                                    "achieved": flops / tsec / 1e12, "peak": c_peak, "unit": "TFLOP/s",
+                                    "frac": flops / tsec / 1e12 / c_peak}, **tens))
+            else:
+                stages.append(dict({"kernel": names[s], "ms": stage_ms[s], "bound": "hbm",
+                                    "achieved": byts / tsec / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                    "frac": byts / tsec / 1e9 / hbm_peak}, **tens))
         elif nst == 4:
             ach = info["alg_bytes"][s] / tsec / 1e9
             stages.append({"kernel": names[s], "ms": stage_ms[s], "bound": "hbm", "achieved": ach,
@@ -316,14 +336,13 @@ def main():
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
                 "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
                 "peak_source": ("%s: %s" % (peaks_src,
-                                            "HBM copy GB/s" if dom["bound"] == "hbm" else
-                                            "bf16 burst x 0.5 (TF32/BF16 nominal) / 3 (3xTF32 split)"))}
+                                            "HBM copy GB/s" if dom["bound"] == "hbm" else c_peak_src))}
     # whole-layer roofline (paper Eq. running-time, stage sum)
     t_roof = 0.0
     if nst == 4:
         for s in range(4):
             tb = info["alg_bytes"][s] / (hbm_peak * 1e9)
-            tc = info["alg_flops"][s] / (tf32_peak / 3.0 * 1e12) if s == 2 else 0.0
+            tc = info["alg_flops"][s] / (c_peak * 1e12) if (s == 2 and c_peak) else 0.0
             t_roof += max(tb, tc)
     layer_frac = (t_roof * 1e3) / ms_step if t_roof else None
 
@@ -379,10 +398,13 @@ def main():
             "config": {"workload": cfg.name, "B_per_gpu": cfg.B, "global_batch": cfg.B * world, "C": cfg.C,
                        "l2_chunk_images": info.get("chunk"), "l2_chunks": info.get("nchunks"),
                        "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": method, "m": m,
-                       "t": info["t"], "gemm": args.gemm if args.gemm != "auto" else "tcgen05_3xtf32",
+                       "t": info["t"], "gemm": gemm_name,
                        "l2": "no flush: inputs %.0f MB/GPU > 126 MB L2" % (I.numel() * 4 / 1e6),
                        "parallelism": "dp%d (batch-sharded ranks, no collective on the data path)" % world,
-                       "arith": "fp32 storage; contraction 3xTF32 on tcgen05 with fp32 TMEM accumulation"},
+                       "arith": ("fp32 storage; contraction %s with fp32 TMEM accumulation" % (
+                           "F16X3 (scaled fp16 hi/lo split, 3 products, kind::f16) on tcgen05"
+                           if gemm_name == "tcgen05_f16x3" else "3xTF32 on tcgen05"
+                           if gemm_name == "tcgen05_3xtf32" else "FFMA"))},
             "roofline": roofline,
             "layer_roofline_frac": layer_frac,
             "stages": stages,

@@ -58,11 +58,23 @@ typedef enum {
     CONV_GAUSS_FFT = 3
 } conv_method;
 
-/* Contraction (NK3) implementation. */
+/* Contraction (NK3) implementation.  Both tcgen05 modes hold fp32 accuracy with
+ * a two-term split of each operand and three tensor-core products (small terms
+ * first), X ~= V_lo U_hi + V_hi U_lo + V_hi U_hi, accumulated in fp32 in TMEM:
+ *   3XTF32  kind::tf32; V_hi = rna_tf32(V), V_lo = V - V_hi, U_hi = trunc_tf32(U)
+ *           (what the MMA reads), U_lo = U - U_hi.  2^-22-relative products.
+ *   F16X3   kind::f16 (2x the tf32 tensor rate): scaled fp16 splits
+ *           a_hi = rn_f16(s a), a_lo = rn_f16(s a - a_hi) with exact power-of-two
+ *           scales -- one per output channel c' for V (from max|W[c']| times the
+ *           transform's norm bound, written by NK1) and one per forward for U
+ *           (from max|U| reduced by NK2) -- removed again in the epilogue; the
+ *           same 22 significant bits as 3xTF32 and no fp16 overflow by construction
+ *           (reading R16). */
 typedef enum {
-    CONV_GEMM_AUTO = 0,            /* tcgen05 3xTF32 */
+    CONV_GEMM_AUTO = 0,            /* tcgen05 F16X3 (the fastest mode that meets the bars) */
     CONV_GEMM_TCGEN05_3XTF32 = 1,  /* tcgen05.mma kind::tf32, TMEM accumulators, hi/lo split */
-    CONV_GEMM_FFMA = 2             /* fp32 FFMA tiled GEMM (the fallback it is measured against) */
+    CONV_GEMM_FFMA = 2,            /* fp32 FFMA tiled GEMM (the fallback it is measured against) */
+    CONV_GEMM_TCGEN05_F16X3 = 3    /* tcgen05.mma kind::f16, scaled fp16 hi/lo split */
 } conv_gemm_impl;
 
 typedef struct conv_plan_s *conv_plan_t;
@@ -93,6 +105,8 @@ typedef struct {
      * stages.  bytes_U / bytes_X / BN_pad above are per chunk. */
     int chunk;          /* images per chunk (== B when not chunked) */
     int nchunks;        /* ceil(B / chunk) */
+    int gemm;           /* the contraction implementation the plan runs (conv_gemm_impl;
+                           CONV_GEMM_AUTO resolved; conv_plan_query reports AUTO's default) */
 } conv_plan_info;
 
 /* Host-only: validate arguments and fill `info` (no CUDA calls).  Errors:
@@ -153,8 +167,13 @@ conv_status conv_forward_cached(conv_plan_t p, const float *in, float *out, void
 conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const float *w, float *out,
                            void *workspace, size_t workspace_bytes, void *stream);
 
-/* Byte offsets of V (hi), V_lo, U and X inside the workspace ([0..3]). */
+/* Byte offsets of V (hi), V_lo, U and X inside the workspace ([0..3]).  V_hi and
+ * V_lo are fp32 (3XTF32 / FFMA) or fp16 (F16X3) [Z][M][Kp] planes. */
 conv_status conv_workspace_layout(conv_plan_t p, size_t offsets[4]);
+/* F16X3 plans: byte offsets of the per-output-channel scales (fp32 [2][C']:
+ * s_v[c'] then 1/s_v[c'], exact powers of two) and of the max|U| word (fp32 bits)
+ * inside the workspace; both 0 for other plans. */
+conv_status conv_workspace_aux(conv_plan_t p, size_t offsets[2]);
 
 /* The plan's Winograd matrices in fp64 (exact rationals): AT [m][t], BT [t][t],
  * G [t][r], so that y = AT[(G g) . (BT d)] (Eq. 1).  UNSUPPORTED for
@@ -167,7 +186,8 @@ const char *conv_status_string(conv_status s);    /* static string, never NULL *
 const char *conv_last_error(void);                /* thread-local detail of the last error */
 
 /* Kernel launches one conv_forward issues for this plan (for gpu_launches):
- * 1 + 3 * nchunks (fast methods) or 1 (direct). */
+ * 1 + 3 * nchunks (fast methods; 2 + 3 * nchunks with F16X3: the NK1 scale
+ * prologue) or 1 (direct).  F16X3 also issues one 4-byte memset per chunk. */
 int conv_forward_launch_count(conv_plan_t p);
 
 /* Per-stage timing without host synchronisation inside a timed loop:

@@ -24,7 +24,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "fastconv.h")
 
 METHODS = {"direct": 0, "winograd": 1, "regular_fft": 2, "gauss_fft": 3}
-GEMMS = {"auto": 0, "tcgen05": 1, "ffma": 2}
+GEMMS = {"auto": 0, "tcgen05": 1, "ffma": 2, "f16x3": 3}
+GEMM_NAMES = {0: "auto", 1: "tcgen05_3xtf32", 2: "ffma", 3: "tcgen05_f16x3"}
 STATUS = {0: "CONV_OK", 1: "CONV_ERR_INVALID_ARG", 2: "CONV_ERR_UNSUPPORTED",
           3: "CONV_ERR_OUT_OF_MEMORY", 4: "CONV_ERR_CUDA", 5: "CONV_ERR_DEVICE_MISMATCH"}
 
@@ -43,7 +44,8 @@ class PlanInfo(ctypes.Structure):
                 [(n, ctypes.c_int) for n in ("gemm_Z", "gemm_M", "gemm_K")] +
                 [(n, ctypes.c_size_t) for n in ("bytes_U", "bytes_V", "bytes_X", "workspace_bytes")] +
                 [("alg_bytes", ctypes.c_double * 4), ("alg_flops", ctypes.c_double * 4),
-                 ("direct_flops", ctypes.c_double), ("chunk", ctypes.c_int), ("nchunks", ctypes.c_int)])
+                 ("direct_flops", ctypes.c_double), ("chunk", ctypes.c_int), ("nchunks", ctypes.c_int),
+                 ("gemm", ctypes.c_int)])
 
     def as_dict(self) -> dict:
         d = {}
@@ -85,6 +87,7 @@ def load(build_if_missing: bool = False):
         "conv_forward_host": ([vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i),
         "conv_run_stage": ([vp, i, vp, vp, vp, vp, sz, vp], i),
         "conv_workspace_layout": ([vp, ctypes.POINTER(sz)], i),
+        "conv_workspace_aux": ([vp, ctypes.POINTER(sz)], i),
         "conv_plan_winograd_matrices": ([vp, dp, dp, dp], i),
         "conv_winograd_matrices": ([i, i, dp, dp, dp], i),
         "conv_destroy": ([vp], None),
@@ -172,6 +175,10 @@ class Plan:
         offs = (ctypes.c_size_t * 4)()
         _check(lib.conv_workspace_layout(h, offs))
         self.layout = {"V": offs[0], "Vlo": offs[1], "U": offs[2], "X": offs[3]}
+        aux = (ctypes.c_size_t * 2)()
+        _check(lib.conv_workspace_aux(h, aux))
+        self.layout.update({"vscale": aux[0], "umax": aux[1]})
+        self.gemm = gemm
         self.launches = int(lib.conv_forward_launch_count(h))
         self.in_shape = (B, C, H, W)
         self.w_shape = (Cout, C, r, r)

@@ -216,7 +216,7 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         fc_set_error("output tile m must be >= 1 (got %d)", m);
         return CONV_ERR_INVALID_ARG;
     }
-    if (gemm < CONV_GEMM_AUTO || gemm > CONV_GEMM_FFMA) {
+    if (gemm < CONV_GEMM_AUTO || gemm > CONV_GEMM_TCGEN05_F16X3) {
         fc_set_error("unknown gemm implementation %d", (int)gemm);
         return CONV_ERR_INVALID_ARG;
     }
@@ -261,12 +261,14 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         } else {
             G.Z = G.E; G.M = Cout; G.K = C;
         }
-        G.Kp = (G.K + 3) / 4 * 4;
+        G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
+        const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
+        G.Kp = (G.K + kq - 1) / kq * kq;
         G.cplx = 0;
-        if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % 16 == 0 &&
+        if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % (G.vf16 ? 32 : 16) == 0 &&
             !getenv("FASTCONV_NO_CPLX")) {
             G.cplx = 1;
-            G.Kp = (C + 3) / 4 * 4;
+            G.Kp = (C + kq - 1) / kq * kq;
         }
     }
     *g = G;
@@ -280,10 +282,13 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         I.direct_flops = 2.0 * B * (double)C * Cout * G.Ho * G.Wo * r * r;
         I.chunk = B;
         I.nchunks = 1;
+        I.gemm = gemm == CONV_GEMM_AUTO ? CONV_GEMM_TCGEN05_F16X3 : gemm;
         if (method != CONV_DIRECT) {
             const int split = (gemm != CONV_GEMM_FFMA);
-            const size_t vb = fc_v_floats(G) * 4;  // V_hi, then V_lo at the next 256 B boundary
+            const size_t vb = fc_v_bytes(G);  // V_hi, then V_lo at the next 256 B boundary
             I.bytes_V = split ? align256(vb) + vb : vb;
+            if (G.vf16)  // + per-c' scales [2][C'] and the max|U| word
+                I.bytes_V = align256(I.bytes_V) + align256((size_t)2 * Cout * 4) + 256;
             I.chunk = pick_chunk(G, I.bytes_V);
             I.nchunks = (B + I.chunk - 1) / I.chunk;
             const Geometry Gc = fc_chunk_geometry(G, I.chunk);
@@ -356,8 +361,8 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
     }
     conv_plan_s *p = (conv_plan_s *)calloc(1, sizeof(conv_plan_s));
     if (!p) return CONV_ERR_OUT_OF_MEMORY;
-    if (gemm == CONV_GEMM_AUTO) gemm = fc_tcgen05_available() ? CONV_GEMM_TCGEN05_3XTF32 : CONV_GEMM_FFMA;
-    if (gemm == CONV_GEMM_TCGEN05_3XTF32 && !fc_tcgen05_available()) {
+    if (gemm == CONV_GEMM_AUTO) gemm = fc_tcgen05_available() ? CONV_GEMM_TCGEN05_F16X3 : CONV_GEMM_FFMA;
+    if ((gemm == CONV_GEMM_TCGEN05_3XTF32 || gemm == CONV_GEMM_TCGEN05_F16X3) && !fc_tcgen05_available()) {
         free(p);
         fc_set_error("tcgen05 contraction not available in this build");
         return CONV_ERR_UNSUPPORTED;
@@ -374,7 +379,17 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
         for (int i = 0; i < g.t * g.t; ++i) cc.BT[i] = (float)p->BT64[i];
         for (int i = 0; i < g.t * g.r; ++i) cc.G[i] = (float)p->G64[i];
         for (int i = 0; i < g.m * g.t; ++i) cc.AT[i] = (float)p->AT64[i];
+        // |V[k][l]| = |sum_pq G[k][p] g[p][q] G[l][q]| <= (max_k sum_p |G[k][p]|)^2 max|g|
+        double rs = 0.0;
+        for (int k = 0; k < g.t; ++k) {
+            double a = 0.0;
+            for (int q = 0; q < g.r; ++q) a += fabs(p->G64[k * g.r + q]);
+            rs = a > rs ? a : rs;
+        }
+        p->g.vbound = (float)(rs * rs);
     } else if (method != CONV_DIRECT) {
+        // |DFT2(pad g)| / t^2 <= r^2 max|g| / t^2; Gauss planes V_i -+ V_r at most twice that
+        p->g.vbound = (float)((method == CONV_GAUSS_FFT ? 2.0 : 1.0) * g.r * g.r / ((double)g.t * g.t));
         for (int j = 0; j < g.t; ++j) {  // twiddles in fp64, rounded once (reading R11)
             const double ang = 2.0 * M_PI * (double)j / (double)g.t;
             cc.cosv[j] = (float)cos(ang);
@@ -408,8 +423,12 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
             return CONV_ERR_CUDA;
         }
         p->off_V = 0;
-        const size_t vb = fc_v_floats(g) * 4;
+        const size_t vb = fc_v_bytes(g);
         p->off_Vlo = align256(vb);
+        if (g.vf16) {
+            p->off_vscale = p->off_Vlo + align256(vb);
+            p->off_umax = p->off_vscale + align256((size_t)2 * g.Cout * 4);
+        }
         const size_t vtot = align256(p->info.bytes_V);
         p->off_U = vtot;
         p->off_X = vtot + align256(p->info.bytes_U);
@@ -477,6 +496,16 @@ conv_status conv_workspace_layout(conv_plan_t p, size_t offsets[4]) {
     return CONV_OK;
 }
 
+conv_status conv_workspace_aux(conv_plan_t p, size_t offsets[2]) {
+    if (!p || !offsets) {
+        fc_set_error("NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    offsets[0] = p->off_vscale;
+    offsets[1] = p->off_umax;
+    return CONV_OK;
+}
+
 conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, double *G) {
     if (!p || !AT || !BT || !G) {
         fc_set_error("NULL argument");
@@ -494,7 +523,7 @@ conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, d
 
 int conv_forward_launch_count(conv_plan_t p) {
     if (!p) return 0;
-    return p->g.method == CONV_DIRECT ? 1 : 1 + 3 * p->nchunks;
+    return p->g.method == CONV_DIRECT ? 1 : (p->g.vf16 ? 2 : 1) + 3 * p->nchunks;
 }
 
 // -- pointer checks ----------------------------------------------------------
@@ -547,24 +576,39 @@ static conv_status launch_result(cudaError_t e, const char *what) {
     return CONV_OK;
 }
 
-static conv_status run_stage(conv_plan_s *p, const Geometry &g, int stage, const float *in, const float *w,
+static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, const float *in, const float *w,
                              float *out, char *ws, cudaStream_t s) {
     float *V = (float *)(ws + p->off_V);
     float *Vlo = p->gemm == CONV_GEMM_FFMA ? nullptr : (float *)(ws + p->off_Vlo);
     float *U = (float *)(ws + p->off_U);
     float *X = (float *)(ws + p->off_X);
+    Geometry g = g0;
+    g.umax = nullptr;
+    g.vscale = nullptr;
+    if (g.vf16) {
+        g.umax = (unsigned int *)(ws + p->off_umax);
+        g.vscale = (float *)(ws + p->off_vscale);
+    }
+    const int split = g.vf16 ? 2 : (Vlo != nullptr);
     switch (stage) {
         case 0: {
+            if (g.vf16) {  // per-c' power-of-two scales before the fp16 split
+                conv_status st = launch_result(fc_launch_vscale(g, w, s), "NK1 scale prologue");
+                if (st) return st;
+            }
             int handled = 0;
             if (!p->generic_transforms) {
-                cudaError_t e = fc_launch_kernel_transform_fast(g, p->host_consts, w, V, Vlo, Vlo != nullptr, s,
-                                                                &handled);
+                cudaError_t e = fc_launch_kernel_transform_fast(g, p->host_consts, w, V, Vlo, split, s, &handled);
                 if (handled) return launch_result(e, "NK1 kernel transform");
             }
-            return launch_result(fc_launch_kernel_transform(g, p->d_consts, w, V, Vlo, Vlo != nullptr, s),
+            return launch_result(fc_launch_kernel_transform(g, p->d_consts, w, V, Vlo, split, s),
                                  "NK1 kernel transform");
         }
         case 1: {
+            if (g.vf16) {  // NK2 reduces max|U| for the contraction's fp16 scale
+                conv_status st = launch_result(cudaMemsetAsync(g.umax, 0, sizeof(unsigned int), s), "max|U| reset");
+                if (st) return st;
+            }
             int handled = 0;
             if (!p->generic_transforms) {
                 cudaError_t e = fc_launch_transform_fast(g, p->host_consts, in, U, 1, s, &handled);
@@ -575,6 +619,8 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g, int stage, const
         case 2:
             if (p->gemm == CONV_GEMM_FFMA)
                 return launch_result(fc_launch_gemm_ffma(g, V, U, X, s), "NK3 FFMA contraction");
+            if (g.vf16)
+                return launch_result(fc_launch_gemm_tcgen05_f16(g, V, Vlo, U, X, s), "NK3 tcgen05 F16X3 contraction");
             return launch_result(fc_launch_gemm_tcgen05(g, V, Vlo, U, X, s), "NK3 tcgen05 contraction");
         case 3: {
             int handled = 0;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <stddef.h>
 
@@ -33,6 +34,14 @@ struct Geometry {
     int cplx;     // Regular-FFT complex mode (tcgen05, C' % 256 == 0, C % 16 == 0): V stored as
                   // (V_r, V_i) planes [E][2][C'][Kp], Kp = round4(C), instead of the 4x real
                   // embedding; the contraction picks the plane per K-half and negates -V_i
+    // F16X3 contraction (conv_gemm_impl CONV_GEMM_TCGEN05_F16X3): V_hi / V_lo are fp16,
+    // Kp = K rounded up to 8 (16-byte rows), scaled per output channel c' by
+    // vscale[c'] = 2^k (inverse at vscale[Cout + c']); NK2 reduces max|U| into *umax
+    // (fp32 bits, reset before every NK2).  Pointers are filled per call (workspace).
+    int vf16;
+    float vbound;            // host bound: max|V[.][c'][.]| <= vbound * max|W[c']|
+    unsigned int *umax;      // NK2 -> NK3 (nullptr: NK2 does not reduce)
+    float *vscale;           // [2][Cout]: NK1 writes, NK3 epilogue reads the inverse
 };
 
 struct conv_plan_s {
@@ -44,16 +53,61 @@ struct conv_plan_s {
     ConvConsts *d_consts;                 // device copy
     int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
+    size_t off_vscale, off_umax;          // F16X3: per-c' scales [2][Cout], max|U| word (else 0)
     int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
     int e2e_chunks;                       // pipelining depth of conv_forward_host
     cudaStream_t h2d, d2h;                // copy streams of the pipelined host path
     conv_plan_info info;
 };
 
-// floats of V (one of V_hi / V_lo)
+// elements of V (one of V_hi / V_lo; fp32, or fp16 in F16X3 mode)
 inline size_t fc_v_floats(const Geometry &g) {
     return g.cplx ? (size_t)2 * g.E * g.Cout * g.Kp : (size_t)g.Z * g.M * g.Kp;
 }
+inline size_t fc_v_bytes(const Geometry &g) { return fc_v_floats(g) * (g.vf16 ? 2 : 4); }
+
+// Block-wide max of non-negative floats into *gmax (fp32 bit patterns order as
+// unsigned integers): warp reduce, shared atomic, one global atomic per CTA.
+// Every thread of the block must call it (no early returns before).
+#ifdef __CUDACC__
+__device__ __forceinline__ void fc_block_umax(unsigned int *gmax, float v) {
+    __shared__ unsigned int s_max;
+    if (threadIdx.x == 0) s_max = 0u;
+    __syncthreads();
+    const unsigned int u = __reduce_max_sync(0xffffffffu, __float_as_uint(v));
+    if ((threadIdx.x & 31) == 0) atomicMax(&s_max, u);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(gmax, s_max);
+}
+// Store one transformed-kernel value V[o]: split 0 = fp32; 1 = 3xTF32 pair
+// (hi = rna_tf32(v), lo = v - hi, fp32); 2 = F16X3 pair of scaled fp16
+// (x = v * sv, hi = rn_f16(x), lo = rn_f16(x - hi)).
+__device__ __forceinline__ void fc_store_v(float *V, float *Vlo, size_t o, float v, int split, float sv) {
+    if (split == 2) {
+        const float x = v * sv;
+        const __half hi = __float2half_rn(x);
+        reinterpret_cast<__half *>(V)[o] = hi;
+        reinterpret_cast<__half *>(Vlo)[o] = __float2half_rn(x - __half2float(hi));
+    } else if (split) {
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+        const float hi = __uint_as_float(r);
+        V[o] = hi;
+        Vlo[o] = v - hi;
+    } else {
+        V[o] = v;
+    }
+}
+// exact power-of-two scale s with max * s in [2^(top-1), 2^top); 1 for 0 / non-finite max
+__device__ __forceinline__ float fc_pow2_scale(float mx, int top) {
+    if (!(mx > 0.f) || !(mx < 3.0e38f)) return 1.f;
+    int ex;
+    frexpf(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
+    int k = top - ex;
+    k = k > 126 ? 126 : (k < -126 ? -126 : k);
+    return ldexpf(1.f, k);
+}
+#endif
 
 // geometry of a chunk of Bc images (U / X row pitch BN_pad follows the chunk)
 Geometry fc_chunk_geometry(const Geometry &g, int Bc);
@@ -75,6 +129,11 @@ cudaError_t fc_launch_gemm_ffma(const Geometry &g, const float *V, const float *
                                 cudaStream_t s);
 cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo,
                                    const float *U, float *X, cudaStream_t s);
+// F16X3: Vhi / Vlo are fp16 planes; scales via g.vscale / g.umax
+cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const void *Vlo,
+                                       const float *U, float *X, cudaStream_t s);
+// F16X3 NK1 prologue: vscale[c'] from max|W[c']| * g.vbound (one CTA per c')
+cudaError_t fc_launch_vscale(const Geometry &g, const float *w, cudaStream_t s);
 cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w, float *out,
                              cudaStream_t s);
 int fc_tcgen05_available();

@@ -32,6 +32,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "common.h"
 
 namespace {
@@ -110,6 +112,13 @@ struct Tc<1> {
             "l"(a), "l"(b), "r"(idesc), "r"(acc)
             : "memory");
     }
+    static __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    }
     static __device__ __forceinline__ void commit(uint32_t bar) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                      : "memory");
@@ -133,6 +142,13 @@ struct Tc<2> {
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+    static __device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(acc)
             : "memory");
     }
@@ -407,6 +423,280 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// F16X3 variant (conv_gemm_impl CONV_GEMM_TCGEN05_F16X3, reading R16):
+// tcgen05.mma kind::f16 (fp16 x fp16 -> fp32, twice the kind::tf32 rate) on
+// scaled two-term fp16 splits, three products per K step as above:
+//     s_v s_u (V.U) ~= V'_lo.U'_hi + V'_hi.U'_lo + V'_hi.U'_hi
+// V' = s_v[c'] V pre-split by NK1 into fp16 (V'_hi, V'_lo) planes, K-major,
+// TMA-loaded with the 64 B swizzle (32 K per row); U arrives as fp32 (NK2's
+// output, read from HBM once per tile) and the four splitter warps write
+// U'_hi = rn_f16(s_u U), U'_lo = rn_f16(s_u U - U'_hi) K-major in the same
+// 64 B-swizzled layout (row = tile column n, 16-byte chunk = 8 K values).
+// s_u = 2^(15 - e) with max|U| < 2^e (NK2's reduction), so |s_u U| < 2^15 and
+// no fp16 overflows; the epilogue multiplies each accumulator row by
+// 1 / (s_u s_v[c']) (exact powers of two) before the TMA store of X.
+template <int CG, int BLOCK_N, int STAGES>
+struct TcCfgF16 {
+    static constexpr int BK = 32;              // K per stage (one 64 B swizzle row of fp16)
+    static constexpr int BM = 128 * CG;
+    static constexpr int NH = BLOCK_N / CG;    // tile columns (n) held per CTA
+    static constexpr int A_BYTES = 128 * BK * 2;
+    static constexpr int UF_BYTES = NH * BK * 4;   // fp32 U as TMA lands it: [BK][NH]
+    static constexpr int B_BYTES = NH * BK * 2;    // one fp16 split plane: [NH][BK] swizzled
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + UF_BYTES + 2 * B_BYTES;
+    static constexpr int TX_BYTES = 2 * A_BYTES + UF_BYTES;
+    static constexpr int TMEM_COLS = 2 * BLOCK_N;
+    static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);  // .x = a (low half), .y = b
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
+
+template <int CG, int BLOCK_N, int STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    nk3_gemm_tcgen05_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
+                         const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, int M,
+                         int K, long long NP, int Z, int cplx, int Mh, int kb_half, int Cout,
+                         const unsigned int *__restrict__ umax_p, const float *__restrict__ inv_sv) {
+    using Cfg = TcCfgF16<CG, BLOCK_N, STAGES>;
+    using I = Tc<CG>;
+    constexpr int BK = Cfg::BK;
+    static_assert(Cfg::TMEM_COLS <= 512, "TMEM holds 512 columns");
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t epi0 = base + STAGES * Cfg::STAGE_BYTES;
+    const uint32_t bar0 = epi0 + Cfg::EPI_BYTES;
+    auto full_bar = [&](int s) { return bar0 + 8u * s; };
+    auto split_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+    auto empty_bar = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
+    auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * STAGES + 2 + a); };
+    uint32_t *tmem_slot =
+        reinterpret_cast<uint32_t *>(gbase + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES + 8 * (3 * STAGES + 4));
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const int grp = blockIdx.x / CG, ngrp = gridDim.x / CG;
+    const int n_m = (M + Cfg::BM - 1) / Cfg::BM;
+    const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
+    const int num_tiles = Z * n_m * n_n;
+    const int num_k = (K + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(split_bar(s), 4 * CG);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar(a), 1);
+            mbar_init(tempty_bar(a), 4 * CG);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAlo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmU) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    }
+    if (warp == 1) I::alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
+    tc_fence_before();
+    I::sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto decode = [&](int T, int &z, int &m0, int &n0) {
+        const int mb = T % n_m, rest = T / n_m;
+        m0 = mb * Cfg::BM;
+        n0 = (rest % n_n) * BLOCK_N;
+        z = rest / n_n;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: V'_hi, V'_lo (fp16) and fp32 U columns of this CTA
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int T = grp; T < num_tiles; T += ngrp) {
+                int z, m0, n0;
+                decode(T, z, m0, n0);
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1);
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sU = sA + 2 * Cfg::A_BYTES;
+                    mbar_expect_tx(full_bar(stage), Cfg::TX_BYTES);
+                    int ak = kb * BK, ar = m0 + 128 * (int)rank, az = z;
+                    if (cplx) {
+                        const int re = m0 < Mh, hi = kb >= kb_half;
+                        ak = (kb - hi * kb_half) * BK;
+                        ar -= re ? 0 : Mh;
+                        az = 2 * z + (re ? hi : 1 - hi);
+                    }
+                    tma_load_3d(sA, &tmA, full_bar(stage), ak, ar, az);
+                    tma_load_3d(sAlo, &tmAlo, full_bar(stage), ak, ar, az);
+                    tma_load_3d(sU, &tmU, full_bar(stage), n0 + (int)rank * Cfg::NH, kb * BK, z);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA)
+            // kind::f16: D f32 (bit 4), A = B = f16 (0), both K-major, N >> 3 at 17, M >> 4 at 24
+            const uint32_t idesc0 = (1u << 4) | ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(Cfg::BM >> 4) << 24);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int T = grp; T < num_tiles; T += ngrp) {
+                mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
+                const bool re_tile = cplx && (T % n_m) * Cfg::BM < Mh;
+                for (int kb = 0; kb < num_k; ++kb) {
+                    mbar_wait(split_bar(stage), phase);
+                    tc_fence_after();
+                    const uint32_t idesc = (re_tile && kb >= kb_half) ? (idesc0 | (1u << 13)) : idesc0;
+                    const uint32_t sA = base + stage * Cfg::STAGE_BYTES;
+                    const uint32_t sAlo = sA + Cfg::A_BYTES;
+                    const uint32_t sB = sA + 2 * Cfg::A_BYTES + Cfg::UF_BYTES;
+                    const uint32_t sBlo = sB + Cfg::B_BYTES;
+#pragma unroll
+                    for (int s = 0; s < BK / 16; ++s) {  // K = 16 per instruction: +32 B in the 64 B row
+                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 512, 4);
+                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 512, 4);
+                        const uint64_t b_hi = make_desc(sB + 32 * s, 16, 512, 4);
+                        const uint64_t b_lo = make_desc(sBlo + 32 * s, 16, 512, 4);
+                        const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
+                        I::mma_f16(d_tmem, a_lo, b_hi, idesc, first);
+                        I::mma_f16(d_tmem, a_hi, b_lo, idesc, 1u);
+                        I::mma_f16(d_tmem, a_hi, b_hi, idesc, 1u);
+                    }
+                    I::commit(empty_bar(stage));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                I::commit(tfull_bar(acc));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---- epilogue: unscale by 1 / (s_u s_v[c']) and TMA-store X (as the tf32 kernel)
+        const int q = warp & 3;
+        const uint32_t stage0 = epi0 + q * (2 * 4096);
+        const float inv_su = 1.f / fc_pow2_scale(__uint_as_float(*umax_p), 15);
+        int acc = 0, buf = 0;
+        uint32_t acc_phase = 0;
+        for (int T = grp; T < num_tiles; T += ngrp) {
+            int z, m0, n0;
+            decode(T, z, m0, n0);
+            const int row0 = m0 + 128 * (int)rank + q * 32;
+            int cp = row0 + lane;
+            cp = cp >= Cout ? cp - Cout : cp;  // rows [C', 2C') of the Regular-FFT products: Im of c'
+            const float rs = cp < Cout ? inv_su * __ldg(inv_sv + cp) : 0.f;
+            mbar_wait(tfull_bar(acc), acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BLOCK_N / 32; ++c) {
+                uint32_t v[32];
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
+                TMEM_LD_32(taddr, v);
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                const uint32_t sb = stage0 + buf * 4096;
+                const uint32_t rowaddr = sb + lane * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + ((j ^ (lane & 7)) << 4)),
+                                 "r"(v[4 * j]), "r"(v[4 * j + 1]), "r"(v[4 * j + 2]), "r"(v[4 * j + 3])
+                                 : "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                            &tmX),
+                        "r"(sb), "r"(n0 + 32 * c), "r"(row0), "r"(z)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                buf ^= 1;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) I::arrive_leader(tempty_bar(acc));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else if (warp >= 8) {
+        // ---- splitter: fp32 U [BK][NH] -> scaled fp16 (hi, lo), K-major 64 B-swizzled rows
+        const int st = threadIdx.x - 256;
+        const float su = fc_pow2_scale(__uint_as_float(*umax_p), 15);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int T = grp; T < num_tiles; T += ngrp) {
+            for (int kb = 0; kb < num_k; ++kb) {
+                mbar_wait(full_bar(stage), phase);
+                const float *uf =
+                    reinterpret_cast<const float *>(gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES);
+                uint8_t *bh = gbase + stage * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::UF_BYTES;
+                uint8_t *bl = bh + Cfg::B_BYTES;
+#pragma unroll
+                for (int i = 0; i < Cfg::NH * BK / 8 / 128; ++i) {
+                    const int chunk = st + 128 * i;
+                    const int n = chunk % Cfg::NH, kg = chunk / Cfg::NH;  // 8 K values kg*8.. of column n
+                    float x[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) x[j] = uf[(kg * 8 + j) * Cfg::NH + n] * su;
+                    uint32_t h[4], l[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        h[j] = pack_half2(x[2 * j], x[2 * j + 1]);
+                        const __half2 hv = *reinterpret_cast<const __half2 *>(&h[j]);
+                        const float2 hf = __half22float2(hv);
+                        l[j] = pack_half2(x[2 * j] - hf.x, x[2 * j + 1] - hf.y);
+                    }
+                    const int off = n * 64 + (((kg ^ (n >> 1)) & 3) << 4);
+                    *reinterpret_cast<uint4 *>(bh + off) = make_uint4(h[0], h[1], h[2], h[3]);
+                    *reinterpret_cast<uint4 *>(bl + off) = make_uint4(l[0], l[1], l[2], l[3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if ((st & 31) == 0) I::arrive_leader(split_bar(stage));
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    I::sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        I::dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -420,14 +710,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_3d(CUtensorMap *map, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
-               uint64_t s2_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz) {
+               uint64_t s2_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz,
+               CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {d0, d1, d2};
     cuuint64_t strides[2] = {s1_bytes, s2_bytes};
     cuuint32_t box[3] = {b0, b1, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+    CUresult r = enc(map, dt, 3, const_cast<void *>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -489,6 +780,63 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     return cudaGetLastError();
 }
 
+
+template <int CG, int BLOCK_N, int STAGES>
+cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, const float *U, float *X,
+                       cudaStream_t s) {
+    using Cfg = TcCfgF16<CG, BLOCK_N, STAGES>;
+    static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory per CTA");
+    CUtensorMap mA, mAlo, mU, mX;
+    const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
+    const uint64_t Kp = (uint64_t)g.Kp;  // fp16 elements, multiple of 8
+    const uint64_t vK = g.cplx ? (uint64_t)g.C : K, vM = g.cplx ? (uint64_t)g.Cout : M;
+    const uint64_t vZ = g.cplx ? 2 * (uint64_t)g.E : Z;
+    if (!encode_3d(&mA, Vhi, vK, vM, vZ, Kp * 2, vM * Kp * 2, Cfg::BK, 128, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+        !encode_3d(&mAlo, Vlo, vK, vM, vZ, Kp * 2, vM * Kp * 2, Cfg::BK, 128, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+        !encode_3d(&mU, U, NP, K, Z, NP * 4, K * NP * 4, Cfg::NH, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, STAGES>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long n_m = (g.M + Cfg::BM - 1) / Cfg::BM;
+    const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
+    const long long tiles = (long long)g.Z * n_m * n_n;
+    const long long groups = tiles < g_num_sms / CG ? tiles : g_num_sms / CG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(CG * groups));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = CG > 1 ? 1 : 0;
+    int M_ = g.M, K_ = g.K, Z_ = g.Z, Cout_ = g.Cout;
+    long long NP_ = g.BN_pad;
+    int cplx_ = g.cplx, Mh_ = g.Cout, kbh_ = (g.C + Cfg::BK - 1) / Cfg::BK;
+    if (g.cplx && (g.Cout % Cfg::BM != 0 || g.C % Cfg::BK != 0)) return cudaErrorInvalidValue;
+    const unsigned int *um = g.umax;
+    const float *isv = g.vscale + g.Cout;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mU, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, Cout_, um, isv);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int fc_tcgen05_available() { return get_encode() != nullptr; }
@@ -500,4 +848,12 @@ cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const fl
     // M > 128: CTA pairs (M = 256 per MMA); M <= 128: single CTAs (M = 128 per MMA)
     if (g.M > 128 && !force_1cta) return launch<2, 256, 6, 16>(g, Vhi, Vlo, U, X, s);
     return launch<1, 256, 4, 16>(g, Vhi, Vlo, U, X, s);
+}
+
+cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const void *Vlo, const float *U, float *X,
+                                       cudaStream_t s) {
+    if (!Vlo || !g.umax || !g.vscale) return cudaErrorInvalidValue;
+    static const int force_1cta = getenv("FASTCONV_TC_1SM") != nullptr;
+    if (g.M > 128 && !force_1cta) return launch_f16<2, 256, 4>(g, Vhi, Vlo, U, X, s);
+    return launch_f16<1, 128, 4>(g, Vhi, Vlo, U, X, s);
 }

@@ -20,10 +20,26 @@
 
 namespace {
 
-__device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+// F16X3 NK1 prologue: one CTA per output channel c' reduces max|W[c'][.][.][.]|
+// (C r^2 contiguous floats) and writes the exact power-of-two scale vscale[c']
+// with vscale * vbound * max|W| < 2^14 (so |V[.][c'][.]| * vscale < 2^14 < fp16 max),
+// and its inverse at vscale[Cout + c'] (the contraction epilogue's unscale).
+__global__ void __launch_bounds__(256) nk1_vscale(Geometry g, const float *__restrict__ w) {
+    __shared__ float s_red[8];
+    const int co = blockIdx.x;
+    const size_t len = (size_t)g.C * g.r * g.r;
+    const float *row = w + (size_t)co * len;
+    float mx = 0.f;
+    for (size_t i = threadIdx.x; i < len; i += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(row + i)));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
+        const float sv = fc_pow2_scale(mx * g.vbound, 14);
+        g.vscale[co] = sv;
+        g.vscale[g.Cout + co] = 1.f / sv;  // exact: sv is a power of two
+    }
 }
 
 // ---------------------------------------------------------------- NK1 ------
@@ -44,15 +60,9 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
     const int co = (int)(idx / g.C), c = (int)(idx % g.C);
     const float *ker = w + idx * r * r;
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
+    const float sv = split == 2 ? g.vscale[co] : 1.f;
     auto store = [&](int z, int row, int col, float v) {
-        const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
-        if (split) {
-            const float hi = tf32_rna(v);
-            V[o] = hi;
-            Vlo[o] = v - hi;
-        } else {
-            V[o] = v;
-        }
+        fc_store_v(V, Vlo, (size_t)z * zstride + (size_t)row * g.Kp + col, v, split, sv);
     };
     if (g.method == CONV_WINOGRAD) {
         float T[8];
@@ -180,6 +190,7 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
     __syncthreads();
     // column pass along the H axis and store; nn fastest for coalescing
     const size_t Kdim = g.K, BNp = g.BN_pad;
+    float umx = 0.f;
     for (int idx = threadIdx.x; idx < TN * E; idx += blockDim.x) {
         const int nn = idx % TN, e = idx / TN;
         const long long n = n0 + nn;
@@ -205,13 +216,16 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
                 U[((size_t)(E + e) * Kdim + c) * BNp + n] = ar;
                 U[((size_t)(2 * E + e) * Kdim + c) * BNp + n] = ai;
             }
+            umx = fmaxf(umx, fabsf(ar) + fabsf(ai));
         } else {
             float a = 0.f;
             const float *zc = s_z + (size_t)nn * t * t + l;
             for (int aa = 0; aa < t; ++aa) a = fmaf(s_BT[k * t + aa], zc[aa * t], a);
             U[((size_t)e * Kdim + c) * BNp + n] = a;
+            umx = fmaxf(umx, fabsf(a));
         }
     }
+    if (g.umax) fc_block_umax(g.umax, umx);
 }
 
 // ---------------------------------------------------------------- NK4 ------
@@ -338,6 +352,11 @@ cudaError_t fc_launch_kernel_transform(const Geometry &g, const ConvConsts *dc, 
     const long long n = (long long)g.C * g.Cout;
     const unsigned blocks = (unsigned)((n + 255) / 256);
     nk1_kernel_transform<<<blocks, 256, 0, s>>>(g, dc, w, V, Vlo, split);
+    return cudaGetLastError();
+}
+
+cudaError_t fc_launch_vscale(const Geometry &g, const float *w, cudaStream_t s) {
+    nk1_vscale<<<(unsigned)g.Cout, 256, 0, s>>>(g, w);
     return cudaGetLastError();
 }
 

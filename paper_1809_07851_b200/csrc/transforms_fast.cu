@@ -36,12 +36,6 @@ struct GMat {
     float G[64];
 };
 
-__device__ __forceinline__ float tf32_rna_f(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
 template <int T, int R>
 __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restrict__ w,
                                                 float *__restrict__ V, float *__restrict__ Vlo, int split) {
@@ -67,7 +61,7 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
         }
     const size_t zstride = (size_t)g.M * g.Kp;
     const size_t off = (size_t)co * g.Kp + c;
-    float *vp = V + off, *lp = Vlo ? Vlo + off : nullptr;
+    const float sv = split == 2 ? g.vscale[co] : 1.f;
 #pragma unroll
     for (int kk = 0; kk < T; ++kk)
 #pragma unroll
@@ -75,15 +69,7 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
             float s = 0.f;
 #pragma unroll
             for (int p = 0; p < R; ++p) s = fmaf((float)tg.G[kk][p], tmp[p][l], s);
-            if (split) {
-                const float hi = tf32_rna_f(s);
-                *vp = hi;
-                *lp = s - hi;
-                lp += zstride;
-            } else {
-                *vp = s;
-            }
-            vp += zstride;
+            fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s, split, sv);
         }
 }
 
@@ -102,13 +88,17 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
 // reads hit L1), U = B^T d B unrolled, t^2 streaming stores along n.  (A
 // shared-memory strip-staged variant measured 2.4x slower on VGG-3.2: with the
 // load and compute phases separated by a CTA barrier too few loads stay in flight.)
-template <int T>
-__global__ void __launch_bounds__(512) nk2_wino(Geometry g, const float *__restrict__ in,
-                                                float *__restrict__ U) {
+// RED: also reduce max|U| into *g.umax (F16X3 contraction scale); 128-thread CTAs
+// capped at 64 registers so the reduction costs no occupancy.
+template <int T, bool RED>
+__global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_wino(Geometry g, const float *__restrict__ in,
+                                                                     float *__restrict__ U) {
     constexpr wtab::Tables tb = wtab::make(2, T - 1);  // B^T as literals (depends on t only)
-    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n_ = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int c = blockIdx.y;
-    if (n >= g.BN) return;
+    if (!RED && n_ >= g.BN) return;
+    const bool valid = n_ < g.BN;
+    const long long n = valid ? n_ : g.BN - 1;  // idle lanes recompute the last tile, store nothing
     const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
     const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
     const int y0 = ti * g.m, x0 = tj * g.m;
@@ -138,6 +128,7 @@ __global__ void __launch_bounds__(512) nk2_wino(Geometry g, const float *__restr
         }
     const size_t estride = (size_t)g.K * g.BN_pad;
     float *dp = U + (size_t)c * g.BN_pad + n;
+    float umx = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k)
 #pragma unroll
@@ -145,9 +136,11 @@ __global__ void __launch_bounds__(512) nk2_wino(Geometry g, const float *__restr
             float s = 0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) s = fmaf((float)tb.BT[k][a], z[a][l], s);
-            *dp = s;  // plain store: U of an L2-resident chunk is re-read by NK3 from L2
+            if (valid) *dp = s;  // plain store: U of an L2-resident chunk is re-read by NK3 from L2
+            if (RED) umx = fmaxf(umx, fabsf(s));
             dp += estride;
         }
+    if (RED) fc_block_umax(g.umax, umx);
 }
 
 
@@ -162,8 +155,8 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
     constexpr int WID = MM + T;  // columns covered by the two tiles
     const long long pidx = (long long)blockIdx.x * 128 + threadIdx.x;
     const int c = blockIdx.y;
-    const long long n = 2 * pidx;
-    if (n >= g.BN) return;
+    const bool valid = 2 * pidx < g.BN;
+    const long long n = valid ? 2 * pidx : 0;
     const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
     const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
     const int y0 = ti * MM, x0 = tj * MM;
@@ -202,6 +195,7 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
     }
     const size_t estride = (size_t)g.K * g.BN_pad;
     float *dp = U + (size_t)c * g.BN_pad + n;
+    float umx = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k)
 #pragma unroll
@@ -212,9 +206,11 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
                 sa = fmaf((float)tb.BT[k][a], zA[a][l], sa);
                 sb = fmaf((float)tb.BT[k][a], zB[a][l], sb);
             }
-            *reinterpret_cast<float2 *>(dp) = make_float2(sa, sb);
+            if (valid) *reinterpret_cast<float2 *>(dp) = make_float2(sa, sb);
+            umx = fmaxf(umx, fmaxf(fabsf(sa), fabsf(sb)));
             dp += estride;
         }
+    if (g.umax) fc_block_umax(g.umax, umx);
 }
 
 // ----------------------------------------------------------- Winograd NK4 ---
@@ -310,17 +306,9 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
         for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
     const float inv = 1.0f / ((float)T * (float)T);
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
+    const float sv = split == 2 ? g.vscale[co] : 1.f;
     auto put = [&](int z, int row, int col, float v) {
-        const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
-        if (split) {
-            uint32_t r;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-            const float hi = __uint_as_float(r);
-            V[o] = hi;
-            Vlo[o] = v - hi;
-        } else {
-            V[o] = v;
-        }
+        fc_store_v(V, Vlo, (size_t)z * zstride + (size_t)row * g.Kp + col, v, split, sv);
     };
 #pragma unroll 1
     for (int l = 0; l < H; ++l) {
@@ -430,6 +418,7 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
     }
     __syncthreads();
     const size_t estride = (size_t)g.K * g.BN_pad;
+    float umx = 0.f;
     for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
         const int nn = it % FTN, l = it / FTN;
         const long long n = n0 + nn;
@@ -441,6 +430,8 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
         }
         fct::fft<T, -1>(z);
         if (n >= g.BN) continue;
+#pragma unroll
+        for (int k = 0; k < T; ++k) umx = fmaxf(umx, fabsf(z[k].x) + fabsf(z[k].y));
         if (g.method == CONV_REGULAR_FFT) {
             float *d0 = U + (size_t)c * g.BN_pad + n;
             float *d1 = U + (size_t)(g.C + c) * g.BN_pad + n;
@@ -462,6 +453,7 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
             }
         }
     }
+    if (g.umax) fc_block_umax(g.umax, umx);
 }
 
 // ---------------------------------------------------------------- FFT NK4 ---
@@ -621,8 +613,13 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
             nk2_wino_pair<T, MM><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
         } else {
             static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
-            const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
-            nk2_wino<T><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst);
+            if (g.umax) {
+                const unsigned nblk = (unsigned)((g.BN + 127) / 128);
+                nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
+            } else {
+                const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
+                nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst);
+            }
         }
     } else {
         // about 256 tiles per CTA: strips of one image, or several whole images

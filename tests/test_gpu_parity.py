@@ -41,13 +41,13 @@ def tol(method, m, r):
     return 1e-5
 
 
-GEMMS = ["ffma", "tcgen05"]
+GEMMS = ["ffma", "tcgen05", "f16x3"]
 
 
 def _gemm_ok(gemm):
-    if gemm == "tcgen05":
+    if gemm in ("tcgen05", "f16x3"):
         try:
-            fc.Plan(1, 4, 4, 8, 8, 3, "winograd", 2, "tcgen05")
+            fc.Plan(1, 4, 4, 8, 8, 3, "winograd", 2, gemm)
         except fc.ConvError as e:
             pytest.skip("tcgen05 path unavailable: %s" % e)
 
@@ -122,17 +122,18 @@ def _full_cases():
             yield name, method, m
 
 
+@pytest.mark.parametrize("gemm", ["auto", "tcgen05"])
 @pytest.mark.parametrize("name,method,m", list(_full_cases()))
-def test_full_size_sampled(name, method, m):
+def test_full_size_sampled(name, method, m, gemm):
     cfg, I, W, idx, Os = _full(name)
-    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)  # bench.py's launch config
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm)  # bench.py's launch config
     x, w = I.cuda(), W.cuda()
     y = p.forward(x, w)
     sel = torch.as_tensor(idx, device="cuda")
     ys = y[sel[:, 0], sel[:, 1], sel[:, 2], sel[:, 3]].double().cpu().numpy()
     assert torch.isfinite(y).all()
     err = rel_err(ys, Os)
-    print("FULL %s %s m=%d err=%.3e" % (name, method, m, err))
+    print("FULL %s %s m=%d %s err=%.3e" % (name, method, m, gemm, err))
     assert err <= tol(method, m, cfg.r)
 
 
@@ -217,7 +218,9 @@ def test_abi_errors_on_gpu():
     assert st == 1
     with pytest.raises(ValueError):
         p.forward(x[:, :2].contiguous(), w)
-    assert p.launches == 4
+    assert p.launches == 5  # auto = F16X3: scale prologue + NK1..NK4
+    assert fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2, "tcgen05").launches == 4
+    assert fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2, "ffma").launches == 4
 
 
 def test_forward_host_and_profiled():
@@ -248,7 +251,7 @@ def test_l2_chunking(method, m, chunk, monkeypatch):
     monkeypatch.setenv("FASTCONV_CHUNK", str(chunk))
     p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
     assert p.info["chunk"] == (chunk if chunk else cfg.B)
-    assert p.launches == 1 + 3 * p.info["nchunks"]
+    assert p.launches == 2 + 3 * p.info["nchunks"]  # auto = F16X3 (scale prologue)
     y = p.forward(I.cuda(), W.cuda())
     torch.cuda.synchronize()
     assert rel_err(y.cpu().double().numpy(), O) <= tol(method, m, cfg.r)
@@ -273,17 +276,18 @@ def test_cached_weight_transform(method, m):
     assert rel_err(y.cpu().double().numpy(), oracle.conv_fp64(I, W)) <= tol(method, m, cfg.r)
 
 
-def test_regular_complex_mode_matches_embedding(monkeypatch):
+@pytest.mark.parametrize("gemm", ["tcgen05", "f16x3"])
+def test_regular_complex_mode_matches_embedding(monkeypatch, gemm):
     """Regular-FFT complex mode ((V_r, V_i) planes, A-negate for -V_i) gives exactly the
     real-embedding result ([[V_r, -V_i], [V_i, V_r]] stored), and both match the oracle."""
-    cfg = synth.custom(2, 48, 256, 18, 18, 3, seed=71, dist="normal")
+    cfg = synth.custom(2, 64, 256, 18, 18, 3, seed=71, dist="normal")
     I, W = synth.make_inputs(cfg)
     O = oracle.conv_fp64(I, W)
     x, w = I.cuda(), W.cuda()
-    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6)
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6, gemm)
     y = p.forward(x, w)
     monkeypatch.setenv("FASTCONV_NO_CPLX", "1")
-    pe = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6)
+    pe = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "regular_fft", 6, gemm)
     ye = pe.forward(x, w)
     torch.cuda.synchronize()
     assert p.info["bytes_V"] < pe.info["bytes_V"]  # half the V bytes

@@ -38,7 +38,7 @@ def _ws_view(ws, off, count):
 
 
 @pytest.mark.parametrize("shape", [(2, 4, 3, 16, 14, 3), (3, 72, 160, 21, 19, 3)])
-@pytest.mark.parametrize("gemm", ["ffma", "tcgen05"])
+@pytest.mark.parametrize("gemm", ["ffma", "tcgen05", "f16x3"])
 @pytest.mark.parametrize("method,m", [("winograd", 2), ("winograd", 4), ("regular_fft", 6), ("gauss_fft", 6),
                                       ("regular_fft", 5)])
 def test_stages(fc, method, m, gemm, shape):
@@ -48,19 +48,35 @@ def test_stages(fc, method, m, gemm, shape):
     info = p.info
     t, h, E, N, BN, BNp = info["t"], info["h"], info["E"], info["N"], info["BN"], info["BN_pad"]
     Z, M, K = info["gemm_Z"], info["gemm_M"], info["gemm_K"]
-    Kp = (K + 3) // 4 * 4
+    Kp = (K + 7) // 8 * 8 if gemm == "f16x3" else (K + 3) // 4 * 4
     x, w = I.cuda(), W.cuda()
     ws = p.alloc_workspace()
     out = torch.empty(p.out_shape, device="cuda")
     p.run_stage(0, w=w, workspace=ws)
     p.run_stage(1, x=x, workspace=ws)
     torch.cuda.synchronize()
-    V = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
+    if gemm == "f16x3":  # scaled fp16 pair: V = (V'_hi + V'_lo) / s_v[c'], s_v a power of two
+        hv = lambda off: ws[off:off + 2 * Z * M * Kp].view(torch.float16).reshape(Z, M, Kp)[:, :, :K]
+        Vh, Vl = hv(p.layout["V"]), hv(p.layout["Vlo"])
+        vs = ws[p.layout["vscale"]:p.layout["vscale"] + 8 * cfg.Cout].view(torch.float32).cpu()
+        sv, inv = vs[:cfg.Cout].double().numpy(), vs[cfg.Cout:].double().numpy()
+        assert np.all(sv * inv == 1.0) and np.all(np.log2(sv) == np.round(np.log2(sv)))
+        assert torch.isfinite(Vh).all() and Vh.abs().max().item() <= 2.0 ** 14
+        rows = np.arange(M) % cfg.Cout
+        V = (Vh.double().cpu().numpy() + Vl.double().cpu().numpy()) * inv[rows][None, :, None]
+    else:
+        V = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
     if gemm == "tcgen05":  # NK1 stores the 3xTF32 split: V = V_hi + V_lo, V_hi exactly TF32
         Vhi = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].cpu()
         assert torch.all((Vhi.view(torch.int32) & 0x1FFF) == 0)
         V = V + _ws_view(ws, p.layout["Vlo"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
     U = _ws_view(ws, p.layout["U"], Z * K * BNp).reshape(Z, K, BNp)[:, :, :BN].double().cpu().numpy()
+    if gemm == "f16x3":  # NK2's reduction: exactly max|U| (Winograd), a bound |re|+|im| (FFT)
+        umax = ws[p.layout["umax"]:p.layout["umax"] + 4].view(torch.float32).item()
+        if method == "winograd":
+            assert umax == np.abs(U).max()
+        else:
+            assert np.abs(U).max() <= umax <= 2.0 * np.abs(U).max()
     In = I.double().numpy()
     Wn = W.double().numpy()
     tiles = _tiles(In, m, cfg.r, info["n_h"], info["n_w"])  # [B][C][N][t][t]
