@@ -523,7 +523,7 @@ conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, d
 
 int conv_forward_launch_count(conv_plan_t p) {
     if (!p) return 0;
-    return p->g.method == CONV_DIRECT ? 1 : (p->g.vf16 ? 2 : 1) + 3 * p->nchunks;
+    return p->g.method == CONV_DIRECT ? 1 : 1 + 3 * p->nchunks;
 }
 
 // -- pointer checks ----------------------------------------------------------
@@ -592,10 +592,6 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, cons
     const int split = g.vf16 ? 2 : (Vlo != nullptr);
     switch (stage) {
         case 0: {
-            if (g.vf16) {  // per-c' power-of-two scales before the fp16 split
-                conv_status st = launch_result(fc_launch_vscale(g, w, s), "NK1 scale prologue");
-                if (st) return st;
-            }
             int handled = 0;
             if (!p->generic_transforms) {
                 cudaError_t e = fc_launch_kernel_transform_fast(g, p->host_consts, w, V, Vlo, split, s, &handled);

@@ -98,6 +98,57 @@ __device__ __forceinline__ void fc_store_v(float *V, float *Vlo, size_t o, float
         V[o] = v;
     }
 }
+// exact power-of-two scale s (declared below)
+__device__ __forceinline__ float fc_pow2_scale(float mx, int top);
+// F16X3: an NK1 CTA owns one output channel c': block-wide max|W[c'][.][.][.]| (C r^2
+// contiguous floats) -> s_v[c'] = 2^k with s_v * vbound * max|W| < 2^14, so every
+// |V[.][c'][.]| * s_v < 2^14 < fp16 max; thread 0 records s_v and 1/s_v (exact).
+// Every thread of the block must call it (once per kernel).
+__device__ __forceinline__ float fc_row_vscale(const Geometry &g, const float *__restrict__ w, int co) {
+    __shared__ float s_red[32];
+    const int len = g.C * g.r * g.r;
+    const float *row = w + (size_t)co * len;
+    float mx = 0.f;
+    // all loads of a round issued before any use (one memory round trip per 8 x blockDim x 4 floats)
+    if ((((uintptr_t)row) & 15) == 0) {
+        const float4 *r4 = reinterpret_cast<const float4 *>(row);
+        const int n4 = len >> 2;
+        for (int b = threadIdx.x; b < n4; b += 8 * blockDim.x) {
+            float4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = b + j * blockDim.x;
+                v[j] = i < n4 ? __ldg(r4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+        }
+        for (int i = (n4 << 2) + threadIdx.x; i < len; i += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(row + i)));
+    } else {
+        for (int b = threadIdx.x; b < len; b += 8 * blockDim.x) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = b + j * blockDim.x;
+                v[j] = i < len ? __ldg(row + i) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx = fmaxf(mx, fabsf(v[j]));
+        }
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
+    const float sv = fc_pow2_scale(mx * g.vbound, 14);
+    if (threadIdx.x == 0 && blockIdx.y == 0) {
+        g.vscale[co] = sv;
+        g.vscale[g.Cout + co] = 1.f / sv;
+    }
+    return sv;
+}
 // exact power-of-two scale s with max * s in [2^(top-1), 2^top); 1 for 0 / non-finite max
 __device__ __forceinline__ float fc_pow2_scale(float mx, int top) {
     if (!(mx > 0.f) || !(mx < 3.0e38f)) return 1.f;
@@ -132,8 +183,6 @@ cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const fl
 // F16X3: Vhi / Vlo are fp16 planes; scales via g.vscale / g.umax
 cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const void *Vlo,
                                        const float *U, float *X, cudaStream_t s);
-// F16X3 NK1 prologue: vscale[c'] from max|W[c']| * g.vbound (one CTA per c')
-cudaError_t fc_launch_vscale(const Geometry &g, const float *w, cudaStream_t s);
 cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w, float *out,
                              cudaStream_t s);
 int fc_tcgen05_available();

@@ -20,28 +20,6 @@
 
 namespace {
 
-// F16X3 NK1 prologue: one CTA per output channel c' reduces max|W[c'][.][.][.]|
-// (C r^2 contiguous floats) and writes the exact power-of-two scale vscale[c']
-// with vscale * vbound * max|W| < 2^14 (so |V[.][c'][.]| * vscale < 2^14 < fp16 max),
-// and its inverse at vscale[Cout + c'] (the contraction epilogue's unscale).
-__global__ void __launch_bounds__(256) nk1_vscale(Geometry g, const float *__restrict__ w) {
-    __shared__ float s_red[8];
-    const int co = blockIdx.x;
-    const size_t len = (size_t)g.C * g.r * g.r;
-    const float *row = w + (size_t)co * len;
-    float mx = 0.f;
-    for (size_t i = threadIdx.x; i < len; i += blockDim.x) mx = fmaxf(mx, fabsf(__ldg(row + i)));
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
-        const float sv = fc_pow2_scale(mx * g.vbound, 14);
-        g.vscale[co] = sv;
-        g.vscale[g.Cout + co] = 1.f / sv;  // exact: sv is a power of two
-    }
-}
-
 // ---------------------------------------------------------------- NK1 ------
 // One thread per (c', c) kernel; lanes run along c so the V stores coalesce.
 __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const ConvConsts *__restrict__ cc,
@@ -55,12 +33,23 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
     }
     for (int i = threadIdx.x; i < 64; i += blockDim.x) s_G[i] = cc->G[i];
     __syncthreads();
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (long long)g.C * g.Cout) return;
-    const int co = (int)(idx / g.C), c = (int)(idx % g.C);
-    const float *ker = w + idx * r * r;
+    int co, c0, cstep;  // F16X3: one CTA per output channel c' (scale first), threads over c
+    float sv = 1.f;
+    if (split == 2) {
+        co = blockIdx.x;
+        sv = fc_row_vscale(g, w, co);
+        c0 = blockIdx.y * blockDim.x + threadIdx.x;  // grid (C', channel blocks)
+        cstep = gridDim.y * blockDim.x;
+    } else {
+        const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (idx >= (long long)g.C * g.Cout) return;
+        co = (int)(idx / g.C);
+        c0 = (int)(idx % g.C);
+        cstep = g.C;
+    }
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
-    const float sv = split == 2 ? g.vscale[co] : 1.f;
+    for (int c = c0; c < g.C; c += cstep) {
+    const float *ker = w + ((size_t)co * g.C + c) * r * r;
     auto store = [&](int z, int row, int col, float v) {
         fc_store_v(V, Vlo, (size_t)z * zstride + (size_t)row * g.Kp + col, v, split, sv);
     };
@@ -78,7 +67,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                 store(k * t + l, co, c, a);
             }
         }
-        return;
+        continue;
     }
     // FFT: DFT2 of the implicitly zero-padded kernel, conj, / t^2
     const float inv = 1.0f / ((float)t * (float)t);
@@ -124,6 +113,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                 store(2 * E + e, co, c, vr + vi);
             }
         }
+    }
     }
 }
 
@@ -350,13 +340,13 @@ int pick_tn(int t) {
 cudaError_t fc_launch_kernel_transform(const Geometry &g, const ConvConsts *dc, const float *w, float *V,
                                        float *Vlo, int split, cudaStream_t s) {
     const long long n = (long long)g.C * g.Cout;
-    const unsigned blocks = (unsigned)((n + 255) / 256);
-    nk1_kernel_transform<<<blocks, 256, 0, s>>>(g, dc, w, V, Vlo, split);
-    return cudaGetLastError();
-}
-
-cudaError_t fc_launch_vscale(const Geometry &g, const float *w, cudaStream_t s) {
-    nk1_vscale<<<(unsigned)g.Cout, 256, 0, s>>>(g, w);
+    if (split == 2) {
+        const int bs = g.C >= 256 ? 256 : (g.C + 31) / 32 * 32;
+        nk1_kernel_transform<<<dim3((unsigned)g.Cout, (unsigned)((g.C + bs - 1) / bs)), bs, 0, s>>>(g, dc, w, V, Vlo,
+                                                                                                  split);
+    } else {
+        nk1_kernel_transform<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, dc, w, V, Vlo, split);
+    }
     return cudaGetLastError();
 }
 

@@ -40,10 +40,24 @@ template <int T, int R>
 __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restrict__ w,
                                                 float *__restrict__ V, float *__restrict__ Vlo, int split) {
     constexpr wtab::Tables tg = wtab::make(T - R + 1, R);  // G as literals
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (long long)g.C * g.Cout) return;
-    const int co = (int)(idx / g.C), c = (int)(idx - (long long)co * g.C);
-    const float *ker = w + idx * (R * R);
+    // F16X3 (split 2): one CTA per output channel c' (its scale first), threads over c;
+    // otherwise one thread per (c', c)
+    int co, c0, cstep;
+    float sv = 1.f;
+    if (split == 2) {
+        co = blockIdx.x;
+        sv = fc_row_vscale(g, w, co);
+        c0 = blockIdx.y * blockDim.x + threadIdx.x;  // grid (C', channel blocks)
+        cstep = gridDim.y * blockDim.x;
+    } else {
+        const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (idx >= (long long)g.C * g.Cout) return;
+        co = (int)(idx / g.C);
+        c0 = (int)(idx - (long long)co * g.C);
+        cstep = g.C;
+    }
+    for (int c = c0; c < g.C; c += cstep) {
+    const float *ker = w + ((size_t)co * g.C + c) * (R * R);
     float k[R][R];
 #pragma unroll
     for (int p = 0; p < R; ++p)
@@ -61,7 +75,6 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
         }
     const size_t zstride = (size_t)g.M * g.Kp;
     const size_t off = (size_t)co * g.Kp + c;
-    const float sv = split == 2 ? g.vscale[co] : 1.f;
 #pragma unroll
     for (int kk = 0; kk < T; ++kk)
 #pragma unroll
@@ -71,6 +84,7 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
             for (int p = 0; p < R; ++p) s = fmaf((float)tg.G[kk][p], tmp[p][l], s);
             fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s, split, sv);
         }
+    }
 }
 
 template <int T, int R>
@@ -78,7 +92,12 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
                             int split, cudaStream_t s) {
     (void)hc;
     const long long n = (long long)g.C * g.Cout;
-    nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w, V, Vlo, split);
+    if (split == 2) {
+        const int bs = g.C >= 256 ? 256 : (g.C + 31) / 32 * 32;
+        nk1_wino<T, R><<<dim3((unsigned)g.Cout, (unsigned)((g.C + bs - 1) / bs)), bs, 0, s>>>(g, w, V, Vlo, split);
+    } else {
+        nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w, V, Vlo, split);
+    }
     return cudaGetLastError();
 }
 
@@ -295,10 +314,22 @@ template <int T, int R>
 __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restrict__ w, float *__restrict__ V,
                                                float *__restrict__ Vlo, int split) {
     constexpr int H = T / 2 + 1;
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (long long)g.C * g.Cout) return;
-    const int co = (int)(idx / g.C), c = (int)(idx - (long long)co * g.C);
-    const float *ker = w + idx * (R * R);
+    int co, c0, cstep;  // as nk1_wino: F16X3 CTAs own one c' (scale first)
+    float sv = 1.f;
+    if (split == 2) {
+        co = blockIdx.x;
+        sv = fc_row_vscale(g, w, co);
+        c0 = blockIdx.y * blockDim.x + threadIdx.x;  // grid (C', channel blocks)
+        cstep = gridDim.y * blockDim.x;
+    } else {
+        const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (idx >= (long long)g.C * g.Cout) return;
+        co = (int)(idx / g.C);
+        c0 = (int)(idx - (long long)co * g.C);
+        cstep = g.C;
+    }
+    for (int c = c0; c < g.C; c += cstep) {
+    const float *ker = w + ((size_t)co * g.C + c) * (R * R);
     float k[R][R];
 #pragma unroll
     for (int p = 0; p < R; ++p)
@@ -306,7 +337,6 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
         for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
     const float inv = 1.0f / ((float)T * (float)T);
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
-    const float sv = split == 2 ? g.vscale[co] : 1.f;
     auto put = [&](int z, int row, int col, float v) {
         fc_store_v(V, Vlo, (size_t)z * zstride + (size_t)row * g.Kp + col, v, split, sv);
     };
@@ -351,12 +381,18 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
             }
         }
     }
+    }
 }
 
 template <int T, int R>
 cudaError_t launch_nk1_fft(const Geometry &g, const float *w, float *V, float *Vlo, int split, cudaStream_t s) {
     const long long n = (long long)g.C * g.Cout;
-    nk1_fft<T, R><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, w, V, Vlo, split);
+    if (split == 2) {
+        const int bs = g.C >= 128 ? 128 : (g.C + 31) / 32 * 32;
+        nk1_fft<T, R><<<dim3((unsigned)g.Cout, (unsigned)((g.C + bs - 1) / bs)), bs, 0, s>>>(g, w, V, Vlo, split);
+    } else {
+        nk1_fft<T, R><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, w, V, Vlo, split);
+    }
     return cudaGetLastError();
 }
 
@@ -594,6 +630,300 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
     return cudaGetLastError();
 }
 
+// ------------------------------------------- Winograd NK2 / NK4, plane pipeline ---
+// Whole (b, c) image planes (NK2) or whole per-plane X columns (NK4) are streamed
+// into shared memory with 1-D TMA bulk copies (cp.async.bulk + mbarrier
+// complete_tx) through an NSLOT-deep ring, so the next planes' loads are in
+// flight while the CTA transforms the current one (the thread-per-tile kernels
+// above keep only a few scattered 4-byte loads per thread in flight).  A CTA
+// loops over groups of G planes (G x N tiles ~ one tile per thread):
+//   NK2  group = (b, channels c0..c0+G-1): one contiguous copy of G H x W planes;
+//        thread per tile computes U = B^T d B from smem (zero outside the image)
+//        and stores the t^2 values along n (coalesced 4-byte lanes).
+//   NK4  group = (c', images b0..b0+G-1): E copies of the G*N contiguous values
+//        X[e][c'][b0 N ...]; thread per tile computes Y = A^T X A and stores its
+//        m x m block straight into the output plane (float4 / float2 rows).
+constexpr int PLANE_SLOTS = 3;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITP_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITP_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <int T, bool RED>
+__global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *__restrict__ in,
+                                                     float *__restrict__ U, int G) {
+    constexpr wtab::Tables tb = wtab::make(2, T - 1);
+    extern __shared__ float4 plane_smem4[];
+    float *sm = reinterpret_cast<float *>(plane_smem4);
+    __shared__ __align__(8) uint64_t bars[PLANE_SLOTS];
+    const int HW = g.H * g.W;
+    const int gpb = (g.C + G - 1) / G;  // channel groups per image
+    const int total = g.B * gpb;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(bars);
+    auto issue = [&](int q, int slot) {
+        const int b = q / gpb, c0 = (q - b * gpb) * G;
+        const int ng = min(G, g.C - c0);
+        const uint32_t bytes = (uint32_t)ng * HW * 4u;
+        mbar_expect(bbase + 8 * slot, bytes);
+        bulk_g2s(sbase + (uint32_t)slot * G * HW * 4u, in + ((size_t)b * g.C + c0) * HW, bytes, bbase + 8 * slot);
+    };
+    if (threadIdx.x == 0) {
+        for (int sl = 0; sl < PLANE_SLOTS; ++sl) mbar_init1(bbase + 8 * sl);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int sl = 0; sl < PLANE_SLOTS; ++sl) {
+            const int q = blockIdx.x + sl * gridDim.x;
+            if (q < total) issue(q, sl);
+        }
+    }
+    __syncthreads();
+    const size_t estride = (size_t)g.K * g.BN_pad;
+    float umx = 0.f;
+    for (int k = 0;; ++k) {
+        const int q = blockIdx.x + k * gridDim.x;
+        if (q >= total) break;
+        const int slot = k % PLANE_SLOTS;
+        mbar_wait_parity(bbase + 8 * slot, (uint32_t)(k / PLANE_SLOTS) & 1u);
+        const int b = q / gpb, c0 = (q - b * gpb) * G;
+        const int ng = min(G, g.C - c0);
+        const float *sp = sm + (size_t)slot * G * HW;
+        for (int it = threadIdx.x; it < ng * g.N; it += blockDim.x) {
+            const int gi = it / g.N, tile = it - gi * g.N;
+            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+            const int y0 = ti * g.m, x0 = tj * g.m;
+            const float *src = sp + gi * HW + y0 * g.W + x0;
+            float d[T][T];
+            if (y0 + T <= g.H && x0 + T <= g.W) {
+#pragma unroll
+                for (int a = 0; a < T; ++a)
+#pragma unroll
+                    for (int qq = 0; qq < T; ++qq) d[a][qq] = src[a * g.W + qq];
+            } else {
+#pragma unroll
+                for (int a = 0; a < T; ++a)
+#pragma unroll
+                    for (int qq = 0; qq < T; ++qq)
+                        d[a][qq] = (y0 + a < g.H && x0 + qq < g.W) ? src[a * g.W + qq] : 0.f;
+            }
+            float z[T][T];
+#pragma unroll
+            for (int a = 0; a < T; ++a)
+#pragma unroll
+                for (int l = 0; l < T; ++l) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int qq = 0; qq < T; ++qq) acc = fmaf((float)tb.BT[l][qq], d[a][qq], acc);
+                    z[a][l] = acc;
+                }
+            float *dp = U + (size_t)(c0 + gi) * g.BN_pad + (size_t)b * g.N + tile;
+#pragma unroll
+            for (int kk = 0; kk < T; ++kk)
+#pragma unroll
+                for (int l = 0; l < T; ++l) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int a = 0; a < T; ++a) acc = fmaf((float)tb.BT[kk][a], z[a][l], acc);
+                    *dp = acc;
+                    if (RED) umx = fmaxf(umx, fabsf(acc));
+                    dp += estride;
+                }
+        }
+        __syncthreads();  // every thread is done with the slot
+        if (threadIdx.x == 0) {
+            const int q2 = blockIdx.x + (k + PLANE_SLOTS) * gridDim.x;
+            if (q2 < total) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(q2, slot);
+            }
+        }
+    }
+    if (RED) fc_block_umax(g.umax, umx);
+}
+
+template <int T, int MM>
+__global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *__restrict__ X,
+                                                     float *__restrict__ out, int G) {
+    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);  // A^T as literals
+    constexpr int E = T * T;
+    extern __shared__ float4 plane_smem4[];
+    float *sm = reinterpret_cast<float *>(plane_smem4);
+    __shared__ __align__(8) uint64_t bars[PLANE_SLOTS];
+    const int gpc = (g.B + G - 1) / G;  // image groups per output channel
+    const int total = g.Cout * gpc;
+    const int GN = G * g.N;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(bars);
+    const size_t estride = (size_t)g.M * g.BN_pad;
+    auto issue = [&](int q, int slot) {  // warp 0: lane j copies elements e = j, j + 32, ...
+        const int co = q / gpc, b0 = (q - co * gpc) * G;
+        const int ng = min(G, g.B - b0);
+        const uint32_t bytes = (uint32_t)ng * g.N * 4u;
+        if (threadIdx.x == 0) mbar_expect(bbase + 8 * slot, bytes * E);
+        __syncwarp();
+        const float *src = X + (size_t)co * g.BN_pad + (size_t)b0 * g.N;
+        for (int e = threadIdx.x; e < E; e += 32)
+            bulk_g2s(sbase + ((uint32_t)slot * E * GN + (uint32_t)e * GN) * 4u, src + e * estride, bytes,
+                     bbase + 8 * slot);
+    };
+    if (threadIdx.x == 0) {
+        for (int sl = 0; sl < PLANE_SLOTS; ++sl) mbar_init1(bbase + 8 * sl);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32)
+        for (int sl = 0; sl < PLANE_SLOTS; ++sl) {
+            const int q = blockIdx.x + sl * gridDim.x;
+            if (q < total) issue(q, sl);
+        }
+    const int vec = (MM % 4 == 0 && g.Wo % 4 == 0) ? 4 : ((MM % 2 == 0 && g.Wo % 2 == 0) ? 2 : 1);
+    for (int k = 0;; ++k) {
+        const int q = blockIdx.x + k * gridDim.x;
+        if (q >= total) break;
+        const int slot = k % PLANE_SLOTS;
+        mbar_wait_parity(bbase + 8 * slot, (uint32_t)(k / PLANE_SLOTS) & 1u);
+        const int co = q / gpc, b0 = (q - co * gpc) * G;
+        const int ng = min(G, g.B - b0);
+        const float *sp = sm + (size_t)slot * E * GN;
+        for (int it = threadIdx.x; it < ng * g.N; it += blockDim.x) {
+            const int gi = it / g.N, tile = it - gi * g.N;
+            float y[MM][MM];
+#pragma unroll
+            for (int a = 0; a < MM; ++a)
+#pragma unroll
+                for (int qq = 0; qq < MM; ++qq) y[a][qq] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < T; ++kk) {
+                float x[T];
+#pragma unroll
+                for (int l = 0; l < T; ++l) x[l] = sp[(kk * T + l) * GN + it];
+#pragma unroll
+                for (int qq = 0; qq < MM; ++qq) {
+                    float rq = 0.f;
+#pragma unroll
+                    for (int l = 0; l < T; ++l) rq = fmaf((float)ta.AT[qq][l], x[l], rq);
+#pragma unroll
+                    for (int a = 0; a < MM; ++a) y[a][qq] = fmaf((float)ta.AT[a][kk], rq, y[a][qq]);
+                }
+            }
+            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+            const int oy = ti * MM, ox = tj * MM;
+            float *op = out + (((size_t)(b0 + gi) * g.Cout + co) * g.Ho + oy) * g.Wo + ox;
+            const bool full_w = ox + MM <= g.Wo;
+#pragma unroll
+            for (int a = 0; a < MM; ++a) {
+                if (oy + a >= g.Ho) break;
+                float *rp = op + (size_t)a * g.Wo;
+                if (full_w && vec == 4) {
+#pragma unroll
+                    for (int qq = 0; qq < MM; qq += 4)
+                        __stcs(reinterpret_cast<float4 *>(rp + qq),
+                               make_float4(y[a][qq], y[a][(qq + 1) % MM], y[a][(qq + 2) % MM], y[a][(qq + 3) % MM]));
+                } else if (full_w && vec == 2) {
+#pragma unroll
+                    for (int qq = 0; qq < MM; qq += 2)
+                        __stcs(reinterpret_cast<float2 *>(rp + qq), make_float2(y[a][qq], y[a][(qq + 1) % MM]));
+                } else {
+#pragma unroll
+                    for (int qq = 0; qq < MM; ++qq)
+                        if (ox + qq < g.Wo) __stcs(rp + qq, y[a][qq]);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int q2 = blockIdx.x + (k + PLANE_SLOTS) * gridDim.x;
+            if (q2 < total) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(q2, slot);
+            }
+        }
+    }
+}
+
+int g_sms_tf = 0;
+int sm_count() {
+    if (!g_sms_tf) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms_tf, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return g_sms_tf;
+}
+
+// plane-pipeline launchers: return false when the geometry does not qualify
+template <int T, int MM>
+bool launch_wino_plane(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s,
+                       cudaError_t *err) {
+    // opt-in (FASTCONV_PLANE=1): on VGG-3.2 F(4,3) it measured NK2 178 us / NK4 145 us
+    // against 150 / 133 us for the thread-per-tile kernels (profiles/r01_summary.md)
+    const bool on = getenv("FASTCONV_PLANE") != nullptr;  // read per launch (tests toggle it)
+    if (!on) return false;
+    const int HW = g.H * g.W;
+    if (forward) {
+        if (HW % 4 != 0 || (size_t)HW * 4 > 48 * 1024) return false;
+        int G = 256 / g.N;
+        G = G < 1 ? 1 : (G > g.C ? g.C : G);
+        while (G > 1 && (size_t)G * HW * 4 > 48 * 1024) --G;
+        const size_t smem = (size_t)PLANE_SLOTS * G * HW * 4;
+        const int per_sm = (int)((200 * 1024) / (smem + 1024)) < 4 ? (int)((200 * 1024) / (smem + 1024)) : 4;
+        const long long total = (long long)g.B * ((g.C + G - 1) / G);
+        long long grid = (long long)sm_count() * (per_sm < 1 ? 1 : per_sm);
+        if (grid > total) grid = total;
+        if (g.umax) {
+            static bool cfg = false;
+            if (!cfg) {
+                cudaFuncSetAttribute(nk2_wino_plane<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cfg = true;
+            }
+            nk2_wino_plane<T, true><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
+        } else {
+            static bool cfg = false;
+            if (!cfg) {
+                cudaFuncSetAttribute(nk2_wino_plane<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                cfg = true;
+            }
+            nk2_wino_plane<T, false><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
+        }
+    } else {
+        const int E = T * T;
+        if (g.N % 4 != 0 || (size_t)E * g.N * 4 > 64 * 1024) return false;
+        int G = 256 / g.N;
+        G = G < 1 ? 1 : (G > g.B ? g.B : G);
+        while (G > 1 && (size_t)E * G * g.N * 4 > 48 * 1024) --G;
+        const size_t smem = (size_t)PLANE_SLOTS * E * G * g.N * 4;
+        int per_sm = (int)((200 * 1024) / (smem + 1024));
+        per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+        const long long total = (long long)g.Cout * ((g.B + G - 1) / G);
+        long long grid = (long long)sm_count() * per_sm;
+        if (grid > total) grid = total;
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(nk4_wino_plane<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cfg = true;
+        }
+        nk4_wino_plane<T, MM><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
+    }
+    *err = cudaGetLastError();
+    return true;
+}
+
 // tile rows per CTA: the staged strip stays within ~32 KB of shared memory
 inline int wino_strip_rows(const Geometry &g, int row_floats) {
     const int per_tile_row = g.m * row_floats * 4;
@@ -606,6 +936,8 @@ inline int wino_strip_rows(const Geometry &g, int row_floats) {
 
 template <int T, int MM>
 cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
+    cudaError_t perr = cudaSuccess;
+    if (launch_wino_plane<T, MM>(g, src, dst, forward, s, &perr)) return perr;
     if (forward) {
         static const int no_pair = getenv("FASTCONV_NK2_PAIR") == nullptr;
         if (g.n_w % 2 == 0 && !no_pair) {

@@ -218,7 +218,7 @@ def test_abi_errors_on_gpu():
     assert st == 1
     with pytest.raises(ValueError):
         p.forward(x[:, :2].contiguous(), w)
-    assert p.launches == 5  # auto = F16X3: scale prologue + NK1..NK4
+    assert p.launches == 4
     assert fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2, "tcgen05").launches == 4
     assert fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2, "ffma").launches == 4
 
@@ -251,7 +251,7 @@ def test_l2_chunking(method, m, chunk, monkeypatch):
     monkeypatch.setenv("FASTCONV_CHUNK", str(chunk))
     p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
     assert p.info["chunk"] == (chunk if chunk else cfg.B)
-    assert p.launches == 2 + 3 * p.info["nchunks"]  # auto = F16X3 (scale prologue)
+    assert p.launches == 1 + 3 * p.info["nchunks"]
     y = p.forward(I.cuda(), W.cuda())
     torch.cuda.synchronize()
     assert rel_err(y.cpu().double().numpy(), O) <= tol(method, m, cfg.r)
@@ -323,3 +323,19 @@ def test_forward_host_pipelined(method, m):
         p.forward_host(hi, hw, ho, di, dw, do, ws)
     torch.cuda.current_stream().synchronize()
     assert torch.equal(ho, ref.cpu())
+
+
+@pytest.mark.parametrize("name", ["tiny", "vgg3_2", "deep"])
+def test_plane_pipeline_transforms(name, monkeypatch):
+    """The opt-in TMA plane-pipeline Winograd NK2 / NK4 (FASTCONV_PLANE=1) give exactly the
+    thread-per-tile kernels' result (same arithmetic, different data movement)."""
+    I, W, O = _reduced(name)
+    for m in (2, 4, 6):
+        if m + W.shape[2] - 1 > 8:
+            continue
+        ref = run_gpu(I, W, "winograd", m)
+        monkeypatch.setenv("FASTCONV_PLANE", "1")
+        y = run_gpu(I, W, "winograd", m)
+        monkeypatch.delenv("FASTCONV_PLANE")
+        assert np.array_equal(y, ref), (name, m)
+        assert rel_err(y, O) <= tol("winograd", m, W.shape[2])
