@@ -68,9 +68,9 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
     for (int p = 0; p < R; ++p)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float s = 0.f;
+            float s = -0.f;
 #pragma unroll
-            for (int q = 0; q < R; ++q) s = fmaf((float)tg.G[l][q], k[p][q], s);
+            for (int q = 0; q < R; ++q) s = wtab::cfma(tg.G[l][q], k[p][q], s);
             tmp[p][l] = s;
         }
     const size_t zstride = (size_t)g.M * g.Kp;
@@ -79,9 +79,9 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
     for (int kk = 0; kk < T; ++kk)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float s = 0.f;
+            float s = -0.f;
 #pragma unroll
-            for (int p = 0; p < R; ++p) s = fmaf((float)tg.G[kk][p], tmp[p][l], s);
+            for (int p = 0; p < R; ++p) s = wtab::cfma(tg.G[kk][p], tmp[p][l], s);
             fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s, split, sv);
         }
     }
@@ -140,9 +140,9 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
     for (int a = 0; a < T; ++a)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float s = 0.f;
+            float s = -0.f;
 #pragma unroll
-            for (int q = 0; q < T; ++q) s = fmaf((float)tb.BT[l][q], d[a][q], s);
+            for (int q = 0; q < T; ++q) s = wtab::cfma(tb.BT[l][q], d[a][q], s);
             z[a][l] = s;
         }
     const size_t estride = (size_t)g.K * g.BN_pad;
@@ -152,9 +152,9 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
     for (int k = 0; k < T; ++k)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float s = 0.f;
+            float s = -0.f;
 #pragma unroll
-            for (int a = 0; a < T; ++a) s = fmaf((float)tb.BT[k][a], z[a][l], s);
+            for (int a = 0; a < T; ++a) s = wtab::cfma(tb.BT[k][a], z[a][l], s);
             if (valid) *dp = s;  // plain store: U of an L2-resident chunk is re-read by NK3 from L2
             if (RED) umx = fmaxf(umx, fabsf(s));
             dp += estride;
@@ -202,11 +202,11 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
         }
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float sa = 0.f, sb = 0.f;
+            float sa = -0.f, sb = -0.f;
 #pragma unroll
             for (int q = 0; q < T; ++q) {
-                sa = fmaf((float)tb.BT[l][q], d[q], sa);
-                sb = fmaf((float)tb.BT[l][q], d[MM + q], sb);
+                sa = wtab::cfma(tb.BT[l][q], d[q], sa);
+                sb = wtab::cfma(tb.BT[l][q], d[MM + q], sb);
             }
             zA[a][l] = sa;
             zB[a][l] = sb;
@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
     for (int k = 0; k < T; ++k)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float sa = 0.f, sb = 0.f;
+            float sa = -0.f, sb = -0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) {
-                sa = fmaf((float)tb.BT[k][a], zA[a][l], sa);
-                sb = fmaf((float)tb.BT[k][a], zB[a][l], sb);
+                sa = wtab::cfma(tb.BT[k][a], zA[a][l], sa);
+                sb = wtab::cfma(tb.BT[k][a], zB[a][l], sb);
             }
             if (valid) *reinterpret_cast<float2 *>(dp) = make_float2(sa, sb);
             umx = fmaxf(umx, fmaxf(fabsf(sa), fabsf(sb)));
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
 #pragma unroll
         for (int a = 0; a < MM; ++a)
 #pragma unroll
-            for (int q = 0; q < MM; ++q) y[a][q] = 0.f;
+            for (int q = 0; q < MM; ++q) y[a][q] = -0.f;
         const float *sp = src0 + tl;
 #pragma unroll
         for (int k = 0; k < T; ++k) {
@@ -273,11 +273,11 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
             if (k & 1) asm volatile("" ::: "memory");  // keep ~2 rows of loads in flight, not all t^2
 #pragma unroll
             for (int q = 0; q < MM; ++q) {
-                float rq = 0.f;
+                float rq = -0.f;
 #pragma unroll
-                for (int l = 0; l < T; ++l) rq = fmaf((float)ta.AT[q][l], x[l], rq);
+                for (int l = 0; l < T; ++l) rq = wtab::cfma(ta.AT[q][l], x[l], rq);
 #pragma unroll
-                for (int a = 0; a < MM; ++a) y[a][q] = fmaf((float)ta.AT[a][k], rq, y[a][q]);
+                for (int a = 0; a < MM; ++a) y[a][q] = wtab::cfma(ta.AT[a][k], rq, y[a][q]);
             }
         }
         const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
@@ -727,9 +727,9 @@ __global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *_
             for (int a = 0; a < T; ++a)
 #pragma unroll
                 for (int l = 0; l < T; ++l) {
-                    float acc = 0.f;
+                    float acc = -0.f;
 #pragma unroll
-                    for (int qq = 0; qq < T; ++qq) acc = fmaf((float)tb.BT[l][qq], d[a][qq], acc);
+                    for (int qq = 0; qq < T; ++qq) acc = wtab::cfma(tb.BT[l][qq], d[a][qq], acc);
                     z[a][l] = acc;
                 }
             float *dp = U + (size_t)(c0 + gi) * g.BN_pad + (size_t)b * g.N + tile;
@@ -737,9 +737,9 @@ __global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *_
             for (int kk = 0; kk < T; ++kk)
 #pragma unroll
                 for (int l = 0; l < T; ++l) {
-                    float acc = 0.f;
+                    float acc = -0.f;
 #pragma unroll
-                    for (int a = 0; a < T; ++a) acc = fmaf((float)tb.BT[kk][a], z[a][l], acc);
+                    for (int a = 0; a < T; ++a) acc = wtab::cfma(tb.BT[kk][a], z[a][l], acc);
                     *dp = acc;
                     if (RED) umx = fmaxf(umx, fabsf(acc));
                     dp += estride;
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *_
 #pragma unroll
             for (int a = 0; a < MM; ++a)
 #pragma unroll
-                for (int qq = 0; qq < MM; ++qq) y[a][qq] = 0.f;
+                for (int qq = 0; qq < MM; ++qq) y[a][qq] = -0.f;
 #pragma unroll
             for (int kk = 0; kk < T; ++kk) {
                 float x[T];
@@ -815,11 +815,11 @@ __global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *_
                 for (int l = 0; l < T; ++l) x[l] = sp[(kk * T + l) * GN + it];
 #pragma unroll
                 for (int qq = 0; qq < MM; ++qq) {
-                    float rq = 0.f;
+                    float rq = -0.f;
 #pragma unroll
-                    for (int l = 0; l < T; ++l) rq = fmaf((float)ta.AT[qq][l], x[l], rq);
+                    for (int l = 0; l < T; ++l) rq = wtab::cfma(ta.AT[qq][l], x[l], rq);
 #pragma unroll
-                    for (int a = 0; a < MM; ++a) y[a][qq] = fmaf((float)ta.AT[a][kk], rq, y[a][qq]);
+                    for (int a = 0; a < MM; ++a) y[a][qq] = wtab::cfma(ta.AT[a][kk], rq, y[a][qq]);
                 }
             }
             const int ti = tile / g.n_w, tj = tile - ti * g.n_w;

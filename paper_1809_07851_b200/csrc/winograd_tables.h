@@ -113,6 +113,17 @@ __host__ __device__ constexpr Tables make(int m, int r) {
     return out;
 }
 
+// acc + c * x for a compile-time coefficient c: after unrolling, c is a literal and
+// the branches fold, so zero coefficients cost nothing and +-1 become an add / sub
+// (fmaf(0, x, acc) itself cannot be dropped under IEEE rules: 0 * inf = NaN).
+// Accumulators start at -0.f, the additive identity that folds (-0 + x == x for all x).
+__device__ __forceinline__ float cfma(double c, float x, float acc) {
+    if (c == 0.0) return acc;
+    if (c == 1.0) return acc + x;
+    if (c == -1.0) return acc - x;
+    return fmaf((float)c, x, acc);
+}
+
 // B^T depends on t only (the point set); A^T on (m, t); G on (r, t).
 template <int T>
 struct BTab {

@@ -28,13 +28,16 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--configs", default="tiny,vgg3_2,vgg1_2,k5,deep")
+    ap.add_argument("--gemm", default="auto", choices=["auto", "f16x3", "tcgen05", "ffma"])
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-    hbm, tc = float(peaks["hbm_gbs"]), float(peaks["bf16_tflops"]) * 0.5 / 3.0
+    hbm = float(peaks["hbm_gbs"])
+    # contraction ceiling of the plans' default (AUTO = F16X3): fp16 dense = bf16 dense, / 3 products
+    tc = float(peaks["bf16_tflops"]) / 3.0 if args.gemm in ("auto", "f16x3") else float(peaks["bf16_tflops"]) * 0.5 / 3.0
     fc.load()
     stream = torch.cuda.current_stream()
-    result = {"device": torch.cuda.get_device_name(0), "steps": args.steps, "configs": {}}
+    result = {"device": torch.cuda.get_device_name(0), "steps": args.steps, "gemm": args.gemm, "configs": {}}
     for name in args.configs.split(","):
         cfg = synth.CONFIGS[name]
         I, W = synth.make_inputs(cfg)
@@ -42,7 +45,7 @@ def main():
         out = torch.empty((cfg.B, cfg.Cout, cfg.Ho, cfg.Wo), device="cuda")
         rows, infos, meas = {}, {}, {}
         for method, m in list(cfg.runs) + [("direct", 0)]:
-            p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+            p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm if method != "direct" else "auto")
             ws = p.alloc_workspace()
             for _ in range(3):
                 p.forward(x, w, out, ws)
