@@ -186,7 +186,8 @@ const char *conv_status_string(conv_status s);    /* static string, never NULL *
 const char *conv_last_error(void);                /* thread-local detail of the last error */
 
 /* Kernel launches one conv_forward issues for this plan (for gpu_launches):
- * 1 + 3 * nchunks (fast methods) or 1 (direct).  F16X3 plans also issue one
+ * 1 + 3 * nchunks (fast methods; 2 + 3 * nchunks for F16X3 FFT plans, whose kernel
+ * transform has a per-c' scale prologue) or 1 (direct).  F16X3 plans also issue one
  * 4-byte memset (the max|U| reset) per chunk. */
 int conv_forward_launch_count(conv_plan_t p);
 

@@ -523,7 +523,10 @@ conv_status conv_plan_winograd_matrices(conv_plan_t p, double *AT, double *BT, d
 
 int conv_forward_launch_count(conv_plan_t p) {
     if (!p) return 0;
-    return p->g.method == CONV_DIRECT ? 1 : 1 + 3 * p->nchunks;
+    if (p->g.method == CONV_DIRECT) return 1;
+    // F16X3 FFT plans run a per-c' scale prologue before the z-sliced FFT kernel transform
+    const int nk1 = (p->g.vf16 && p->g.method != CONV_WINOGRAD && !p->generic_transforms) ? 2 : 1;
+    return nk1 + 3 * p->nchunks;
 }
 
 // -- pointer checks ----------------------------------------------------------

@@ -98,6 +98,14 @@ __device__ __forceinline__ void fc_store_v(float *V, float *Vlo, size_t o, float
         V[o] = v;
     }
 }
+// Two adjacent values V[o], V[o+1] (o even) of the F16X3 pair as half2 stores.
+__device__ __forceinline__ void fc_store_v2(float *V, float *Vlo, size_t o, float v0, float v1, float sv) {
+    const float x0 = v0 * sv, x1 = v1 * sv;
+    const __half2 hi = __floats2half2_rn(x0, x1);
+    const float2 hf = __half22float2(hi);
+    reinterpret_cast<__half2 *>(V)[o >> 1] = hi;
+    reinterpret_cast<__half2 *>(Vlo)[o >> 1] = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+}
 // exact power-of-two scale s (declared below)
 __device__ __forceinline__ float fc_pow2_scale(float mx, int top);
 // F16X3: an NK1 CTA owns one output channel c': block-wide max|W[c'][.][.][.]| (C r^2

@@ -36,67 +36,77 @@ struct GMat {
     float G[64];
 };
 
-template <int T, int R>
+// NC channels per thread: 1 (fp32 / 3xTF32 stores, 128 B per warp store) or 2 (F16X3:
+// the pair (c, c+1) written as half2 so a warp store still covers 128 B).
+template <int T, int R, int NC>
 __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restrict__ w,
                                                 float *__restrict__ V, float *__restrict__ Vlo, int split) {
     constexpr wtab::Tables tg = wtab::make(T - R + 1, R);  // G as literals
-    // F16X3 (split 2): one CTA per output channel c' (its scale first), threads over c;
-    // otherwise one thread per (c', c)
-    int co, c0, cstep;
+    // F16X3 (split 2): CTAs own one output channel c' (its scale first) x a block of channel
+    // pairs; otherwise one thread per (c', c)
+    int co, c;
     float sv = 1.f;
     if (split == 2) {
         co = blockIdx.x;
         sv = fc_row_vscale(g, w, co);
-        c0 = blockIdx.y * blockDim.x + threadIdx.x;  // grid (C', channel blocks)
-        cstep = gridDim.y * blockDim.x;
+        c = NC * (blockIdx.y * blockDim.x + threadIdx.x);
+        if (c >= g.C) return;
     } else {
         const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
         if (idx >= (long long)g.C * g.Cout) return;
         co = (int)(idx / g.C);
-        c0 = (int)(idx - (long long)co * g.C);
-        cstep = g.C;
+        c = (int)(idx - (long long)co * g.C);
     }
-    for (int c = c0; c < g.C; c += cstep) {
-    const float *ker = w + ((size_t)co * g.C + c) * (R * R);
-    float k[R][R];
+    float tmp[NC][R][T];  // tmp[p][l] = sum_q k[p][q] G[l][q]
 #pragma unroll
-    for (int p = 0; p < R; ++p)
+    for (int j = 0; j < NC; ++j) {
+        float k[R][R];
+        const bool ok = c + j < g.C;
+        const float *ker = w + ((size_t)co * g.C + c + j) * (R * R);
 #pragma unroll
-        for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
-    float tmp[R][T];  // tmp[p][l] = sum_q k[p][q] G[l][q]
+        for (int p = 0; p < R; ++p)
 #pragma unroll
-    for (int p = 0; p < R; ++p)
+            for (int q = 0; q < R; ++q) k[p][q] = ok ? __ldg(ker + p * R + q) : 0.f;
 #pragma unroll
-        for (int l = 0; l < T; ++l) {
-            float s = -0.f;
+        for (int p = 0; p < R; ++p)
 #pragma unroll
-            for (int q = 0; q < R; ++q) s = wtab::cfma(tg.G[l][q], k[p][q], s);
-            tmp[p][l] = s;
-        }
+            for (int l = 0; l < T; ++l) {
+                float s = -0.f;
+#pragma unroll
+                for (int q = 0; q < R; ++q) s = wtab::cfma(tg.G[l][q], k[p][q], s);
+                tmp[j][p][l] = s;
+            }
+    }
     const size_t zstride = (size_t)g.M * g.Kp;
     const size_t off = (size_t)co * g.Kp + c;
 #pragma unroll
     for (int kk = 0; kk < T; ++kk)
 #pragma unroll
         for (int l = 0; l < T; ++l) {
-            float s = -0.f;
+            float s[NC];
 #pragma unroll
-            for (int p = 0; p < R; ++p) s = wtab::cfma(tg.G[kk][p], tmp[p][l], s);
-            fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s, split, sv);
+            for (int j = 0; j < NC; ++j) {
+                s[j] = -0.f;
+#pragma unroll
+                for (int p = 0; p < R; ++p) s[j] = wtab::cfma(tg.G[kk][p], tmp[j][p][l], s[j]);
+            }
+            if (NC == 2)
+                fc_store_v2(V, Vlo, off + (size_t)(kk * T + l) * zstride, s[0], s[NC - 1], sv);
+            else
+                fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s[0], split, sv);
         }
-    }
 }
-
 template <int T, int R>
 cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float *w, float *V, float *Vlo,
                             int split, cudaStream_t s) {
     (void)hc;
     const long long n = (long long)g.C * g.Cout;
-    if (split == 2) {
-        const int bs = g.C >= 256 ? 256 : (g.C + 31) / 32 * 32;
-        nk1_wino<T, R><<<dim3((unsigned)g.Cout, (unsigned)((g.C + bs - 1) / bs)), bs, 0, s>>>(g, w, V, Vlo, split);
+    if (split == 2) {  // channel pairs (Kp is a multiple of 8: the pad column absorbs an odd C)
+        const int np = (g.C + 1) / 2;
+        const int bs = np >= 256 ? 256 : (np + 31) / 32 * 32;
+        nk1_wino<T, R, 2><<<dim3((unsigned)g.Cout, (unsigned)((np + bs - 1) / bs)), bs, 0, s>>>(g, w, V, Vlo, split);
     } else {
-        nk1_wino<T, R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w, V, Vlo, split);
+        nk1_wino<T, R, 1><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, w, V, Vlo, split);
     }
     return cudaGetLastError();
 }
@@ -232,6 +242,26 @@ __global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__
     if (g.umax) fc_block_umax(g.umax, umx);
 }
 
+// Copy `rows` staged output rows (pitch SWo floats in smem) to `rows` contiguous rows
+// of Wo floats in global memory: one warp per row, lanes along the row (coalesced,
+// streaming stores, no per-element division).
+__device__ __forceinline__ void store_strip(float *__restrict__ dst, const float *__restrict__ src, int rows, int Wo,
+                                            int SWo) {
+    if (Wo < 48) {  // narrow rows: flat index (one division per element) keeps every lane busy
+        for (int idx = threadIdx.x; idx < rows * Wo; idx += blockDim.x) {
+            const int r = idx / Wo, c = idx - r * Wo;
+            __stcs(dst + idx, src[r * SWo + c]);
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int r = threadIdx.x >> 5; r < rows; r += nw) {
+        const float *sr = src + (size_t)r * SWo;
+        float *dr = dst + (size_t)r * Wo;
+        for (int c = lane; c < Wo; c += 32) __stcs(dr + c, sr[c]);
+    }
+}
+
 // ----------------------------------------------------------- Winograd NK4 ---
 // CTA = (strip of R tile rows, output channel c', image b).  One thread per tile
 // loads its t^2 elements of X along n, computes Y = A^T X A, and writes the m x m
@@ -283,9 +313,21 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
         const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
         float *q0 = so + ti * m * SWo + tj * m;
 #pragma unroll
-        for (int a = 0; a < MM; ++a)
+        for (int a = 0; a < MM; ++a) {
+            if (MM % 4 == 0 && (SWo & 3) == 0) {  // 16-byte rows: conflict-free vector stores
 #pragma unroll
-            for (int q = 0; q < MM; ++q) q0[a * SWo + q] = y[a][q];
+                for (int q = 0; q < MM; q += 4)
+                    *reinterpret_cast<float4 *>(q0 + a * SWo + q) =
+                        make_float4(y[a][q], y[a][(q + 1) % MM], y[a][(q + 2) % MM], y[a][(q + 3) % MM]);
+            } else if (MM % 2 == 0 && (SWo & 1) == 0) {
+#pragma unroll
+                for (int q = 0; q < MM; q += 2)
+                    *reinterpret_cast<float2 *>(q0 + a * SWo + q) = make_float2(y[a][q], y[a][(q + 1) % MM]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < MM; ++q) q0[a * SWo + q] = y[a][q];
+            }
+        }
     }
     __syncthreads();
     const int y0 = i0 * m;
@@ -296,12 +338,15 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
         if (SWo == g.Wo) {
             for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) __stcs(dst + idx, src[idx]);
         } else {
-            for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) {
-                const int row = idx / g.Wo, col = idx - row * g.Wo;
-                __stcs(dst + idx, src[row * SWo + col]);
-            }
+            store_strip(dst, src, orows, g.Wo, SWo);
         }
     }
+}
+
+// F16X3 scale prologue for the z-sliced FFT NK1: one CTA per output channel c'
+// (fc_row_vscale: max|W[c']| -> s_v[c'], 1/s_v[c']).
+__global__ void __launch_bounds__(256) nk1_row_scale(Geometry g, const float *__restrict__ w) {
+    fc_row_vscale(g, w, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- FFT NK1 ---
@@ -310,88 +355,105 @@ __global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, i
 // unrolled for compile-time (t, r) with constant-memory twiddles; the real
 // embedding (Regular) or the Gauss pre-sums and the 3xTF32 split are written
 // along c (coalesced).
-template <int T, int R>
+template <int T, int R, int NC>
 __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restrict__ w, float *__restrict__ V,
                                                float *__restrict__ Vlo, int split) {
     constexpr int H = T / 2 + 1;
-    int co, c0, cstep;  // as nk1_wino: F16X3 CTAs own one c' (scale first)
-    float sv = 1.f;
-    if (split == 2) {
-        co = blockIdx.x;
-        sv = fc_row_vscale(g, w, co);
-        c0 = blockIdx.y * blockDim.x + threadIdx.x;  // grid (C', channel blocks)
-        cstep = gridDim.y * blockDim.x;
-    } else {
-        const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-        if (idx >= (long long)g.C * g.Cout) return;
-        co = (int)(idx / g.C);
-        c0 = (int)(idx - (long long)co * g.C);
-        cstep = g.C;
-    }
-    for (int c = c0; c < g.C; c += cstep) {
-    const float *ker = w + ((size_t)co * g.C + c) * (R * R);
-    float k[R][R];
-#pragma unroll
-    for (int p = 0; p < R; ++p)
-#pragma unroll
-        for (int q = 0; q < R; ++q) k[p][q] = __ldg(ker + p * R + q);
+    // one thread per (c', NC channels) and one half-spectrum column l per grid z-slice;
+    // F16X3's per-c' scale comes from nk1_row_scale (launched first), not from an
+    // in-CTA reduction that every z-slice would repeat.  NC = 2: half2 pair stores.
+    const int npc = (g.C + NC - 1) / NC;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)npc * g.Cout) return;
+    const int co = (int)(idx / npc), c = NC * (int)(idx - (long long)co * npc);
+    const float sv = split == 2 ? g.vscale[co] : 1.f;
+    const int l = blockIdx.z;
     const float inv = 1.0f / ((float)T * (float)T);
-    const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
-    auto put = [&](int z, int row, int col, float v) {
-        fc_store_v(V, Vlo, (size_t)z * zstride + (size_t)row * g.Kp + col, v, split, sv);
-    };
-#pragma unroll 1
-    for (int l = 0; l < H; ++l) {
-        cf tr[R];  // row DFT along q: sum_q g[p][q] W^{-l q}
+    cf tr[NC][R];  // row DFT along q: sum_q g[p][q] W^{-l q}
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        float k[R][R];
+        const bool ok = c + j < g.C;
+        const float *ker = w + ((size_t)co * g.C + c + j) * (R * R);
+#pragma unroll
+        for (int p = 0; p < R; ++p)
+#pragma unroll
+            for (int q = 0; q < R; ++q) k[p][q] = ok ? __ldg(ker + p * R + q) : 0.f;
 #pragma unroll
         for (int p = 0; p < R; ++p) {
             float ar = k[p][0], ai = 0.f;
 #pragma unroll
             for (int q = 1; q < R; ++q) {
-                const int j = (l * q) % T;
-                const float2 tw = fct::c_tw[fct::tw_base(T) + j];
+                const int jj = (l * q) % T;
+                const float2 tw = fct::c_tw[fct::tw_base(T) + jj];
                 ar = fmaf(k[p][q], tw.x, ar);
                 ai = fmaf(-k[p][q], tw.y, ai);
             }
-            tr[p] = cf{ar, ai};
+            tr[j][p] = cf{ar, ai};
         }
+    }
+    const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
+    auto put = [&](int z, int row, int col, const float *v) {
+        const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
+        if (NC == 2)
+            fc_store_v2(V, Vlo, o, v[0], v[NC - 1], sv);
+        else
+            fc_store_v(V, Vlo, o, v[0], split, sv);
+    };
 #pragma unroll
-        for (int kk = 0; kk < T; ++kk) {
-            cf acc = tr[0];
+    for (int kk = 0; kk < T; ++kk) {
+        float vr[NC], vi[NC], t0[NC], t1[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            cf acc = tr[j][0];
 #pragma unroll
             for (int p = 1; p < R; ++p) {
-                const cf t = fct::twiddle_mul<T, -1>(tr[p], kk * p);
+                const cf t = fct::twiddle_mul<T, -1>(tr[j][p], kk * p);
                 acc.x += t.x;
                 acc.y += t.y;
             }
-            const float vr = acc.x * inv, vi = -acc.y * inv;  // conj(DFT) / t^2
-            const int e = kk * H + l;
-            if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
-                put(2 * e, co, c, vr);
-                put(2 * e + 1, co, c, vi);
-            } else if (g.method == CONV_REGULAR_FFT) {  // real embedding [[V_r, -V_i], [V_i, V_r]]
-                put(e, co, c, vr);
-                put(e, co, g.C + c, -vi);
-                put(e, g.Cout + co, c, vi);
-                put(e, g.Cout + co, g.C + c, vr);
-            } else {  // Gauss: V_r, V_i - V_r, V_r + V_i
-                put(e, co, c, vr);
-                put(g.E + e, co, c, vi - vr);
-                put(2 * g.E + e, co, c, vr + vi);
-            }
+            vr[j] = acc.x * inv;  // conj(DFT) / t^2
+            vi[j] = -acc.y * inv;
         }
-    }
+        const int e = kk * H + l;
+        if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
+            put(2 * e, co, c, vr);
+            put(2 * e + 1, co, c, vi);
+        } else if (g.method == CONV_REGULAR_FFT) {  // real embedding [[V_r, -V_i], [V_i, V_r]]
+#pragma unroll
+            for (int j = 0; j < NC; ++j) t0[j] = -vi[j];
+            put(e, co, c, vr);
+            put(e, co, g.C + c, t0);
+            put(e, g.Cout + co, c, vi);
+            put(e, g.Cout + co, g.C + c, vr);
+        } else {  // Gauss: V_r, V_i - V_r, V_r + V_i
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                t0[j] = vi[j] - vr[j];
+                t1[j] = vr[j] + vi[j];
+            }
+            put(e, co, c, vr);
+            put(g.E + e, co, c, t0);
+            put(2 * g.E + e, co, c, t1);
+        }
     }
 }
 
 template <int T, int R>
 cudaError_t launch_nk1_fft(const Geometry &g, const float *w, float *V, float *Vlo, int split, cudaStream_t s) {
     const long long n = (long long)g.C * g.Cout;
+    constexpr int H = T / 2 + 1;
     if (split == 2) {
-        const int bs = g.C >= 128 ? 128 : (g.C + 31) / 32 * 32;
-        nk1_fft<T, R><<<dim3((unsigned)g.Cout, (unsigned)((g.C + bs - 1) / bs)), bs, 0, s>>>(g, w, V, Vlo, split);
+        nk1_row_scale<<<(unsigned)g.Cout, 256, 0, s>>>(g, w);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    // F16X3 with even C: channel pairs (the real embedding's second column block starts at C)
+    if (split == 2 && g.C % 2 == 0) {
+        const long long np = (long long)(g.C / 2) * g.Cout;
+        nk1_fft<T, R, 2><<<dim3((unsigned)((np + 127) / 128), 1, H), 128, 0, s>>>(g, w, V, Vlo, split);
     } else {
-        nk1_fft<T, R><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(g, w, V, Vlo, split);
+        nk1_fft<T, R, 1><<<dim3((unsigned)((n + 127) / 128), 1, H), 128, 0, s>>>(g, w, V, Vlo, split);
     }
     return cudaGetLastError();
 }
@@ -563,11 +625,21 @@ __global__ void __launch_bounds__(512) nk4_fft(Geometry g, int R, int IPC, int S
         fct::fft<T, +1>(z);
         const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts tile rows across the CTA's images
         float *q0 = so + (size_t)(ti * m + a0) * SWo + tj * m;
+        if ((m & 1) == 0 && (SWo & 1) == 0) {  // 8-byte aligned pairs
 #pragma unroll
-        for (int q = 0; q < T; ++q) {
-            if (q < m) {
-                q0[q] = z[q].x;
-                if (has1) q0[SWo + q] = z[q].y;
+            for (int q = 0; q + 1 < T; q += 2) {
+                if (q < m) {
+                    *reinterpret_cast<float2 *>(q0 + q) = make_float2(z[q].x, z[q + 1].x);
+                    if (has1) *reinterpret_cast<float2 *>(q0 + SWo + q) = make_float2(z[q].y, z[q + 1].y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < T; ++q) {
+                if (q < m) {
+                    q0[q] = z[q].x;
+                    if (has1) q0[SWo + q] = z[q].y;
+                }
             }
         }
     }
@@ -577,10 +649,7 @@ __global__ void __launch_bounds__(512) nk4_fft(Geometry g, int R, int IPC, int S
     for (int im = 0; im < nimg; ++im) {
         float *dst = out + (((size_t)(b + im) * g.Cout + co) * g.Ho + y0) * g.Wo;
         const float *src = so + (size_t)im * ntr * m * SWo;
-        for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) {
-            const int row = idx / g.Wo, col = idx - row * g.Wo;
-            __stcs(dst + idx, src[row * SWo + col]);
-        }
+        store_strip(dst, src, orows, g.Wo, SWo);
     }
 }
 

@@ -251,7 +251,7 @@ def test_l2_chunking(method, m, chunk, monkeypatch):
     monkeypatch.setenv("FASTCONV_CHUNK", str(chunk))
     p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
     assert p.info["chunk"] == (chunk if chunk else cfg.B)
-    assert p.launches == 1 + 3 * p.info["nchunks"]
+    assert p.launches == (1 if method == "winograd" else 2) + 3 * p.info["nchunks"]  # F16X3 FFT: scale prologue
     y = p.forward(I.cuda(), W.cuda())
     torch.cuda.synchronize()
     assert rel_err(y.cpu().double().numpy(), O) <= tol(method, m, cfg.r)
