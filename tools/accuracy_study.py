@@ -28,6 +28,8 @@ RUNS = {"winograd": (2, 3, 4, 5, 6), "regular_fft": (2, 4, 6, 8, 14, 22, 30), "g
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--gemm", default="auto", choices=["auto", "f16x3", "tcgen05", "ffma"])
+    ap.add_argument("--out", default=None, help="also copy the JSON here (e.g. gpurun_out/)")
     args = ap.parse_args()
     fc.load()
     out = {}
@@ -45,15 +47,19 @@ def main():
                     continue
                 if method != "direct" and (t > 64 or m > cfg.Ho):
                     continue
-                p = fc.Plan(nb, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+                p = fc.Plan(nb, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m,
+                            args.gemm if method != "direct" else "auto")
                 y = p.forward(x, w).double().cpu().numpy()
                 res["%s/m=%d" % (method, m)] = {
                     "t": t, "max_rel": float(np.abs(y - O).max() / np.abs(O).max()),
                     "l2_rel": float(np.linalg.norm(y - O) / np.linalg.norm(O))}
         out[name] = res
         print(name, {k: "%.2e" % v["max_rel"] for k, v in res.items()}, flush=True)
-    path = os.path.join(ROOT, "profiles", "%s_accuracy.json" % args.tag)
+    out["_gemm"] = args.gemm
+    path = os.path.join(ROOT, "profiles", "%s_accuracy_%s.json" % (args.tag, args.gemm))
     json.dump(out, open(path, "w"), indent=1)
+    if args.out:
+        json.dump(out, open(os.path.join(args.out, os.path.basename(path)), "w"), indent=1)
     print("wrote", path)
 
 
