@@ -268,7 +268,7 @@ __device__ __forceinline__ void store_strip(float *__restrict__ dst, const float
 // block into a shared-memory output strip; the CTA then stores the strip's
 // contiguous output rows with coalesced writes (crop to Ho x Wo on the way).
 template <int T, int MM>
-__global__ void __launch_bounds__(256, 3) nk4_wino(Geometry g, int R, int IPC, int SWo,
+__global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, int SWo,
                                                 const float *__restrict__ X, float *__restrict__ out) {
     constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);  // A^T as literals
     extern __shared__ float so[];  // [img][ntr*m][SWo]
