@@ -468,7 +468,7 @@ struct FftCfg {
 };
 
 template <int T>
-__global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U) {
+__global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U) {
     constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
     extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
     const int c = blockIdx.y;
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(256) nk2_fft(Geometry g, const float *__restri
 // reading R7), cropped m x m block into a shared-memory output strip.  Phase C:
 // coalesced streaming stores of each image's output rows.
 template <int T>
-__global__ void __launch_bounds__(512) nk4_fft(Geometry g, int R, int IPC, int SWo, const float *__restrict__ X,
+__global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, int R, int IPC, int SWo, const float *__restrict__ X,
                                                float *__restrict__ out) {
     constexpr int H = FftCfg<T>::H;
     const int m = g.m;
