@@ -366,6 +366,27 @@ def main():
                   "api": "conv_transform_weights once + conv_forward_cached (NK2-NK4) per step"}
         del ws_c
 
+    # ---- the same forward replayed as a CUDA graph of 10 steps (conv_graph_*) --------
+    graph = None
+    try:
+        gr = plan.capture(x, w, out, ws, steps=10)
+        for _ in range(2):
+            gr.launch(stream)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        g0.record(stream)
+        ng = max(5, args.steps // 10)
+        for _ in range(ng):
+            gr.launch(stream)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = parallel.max_over_ranks(g0.elapsed_time(g1) / (10 * ng), dev)
+        graph = {"ms_per_step": gms, "value": cfg.direct_flops * world / (gms * 1e-3) / 1e12, "unit": UNIT,
+                 "api": "conv_graph_create(steps=10) once + conv_graph_launch per 10 steps"}
+        del gr
+    except Exception as exc:  # reported, never fatal to the bench line
+        graph = {"error": str(exc)[:200]}
+
     # ---- end to end through the public API (host buffers, copies in the region) ---
     e2e = None
     if nst == 4 or True:
@@ -411,6 +432,7 @@ def main():
             "sweep": sweep,
             "planner": plan_report,
             "inference_cached_weights": cached,
+            "cuda_graph": graph,
             "cpu_baseline": cpu,
             "clocks": clk,
             "e2e": e2e,

@@ -206,6 +206,20 @@ conv_status conv_timer_read(conv_timer_t t, float stage_ms[4], int *launches);
 void conv_timer_reset(conv_timer_t t);
 void conv_timer_destroy(conv_timer_t t);   /* NULL-safe */
 
+/* CUDA graphs of the forward pass (launch-bound layers, fixed buffers):
+ * conv_graph_create() captures `steps` consecutive conv_forward() calls (or, with
+ * cached != 0, conv_forward_cached() calls reading the V already in `workspace`)
+ * on the given device buffers into one instantiated CUDA graph; conv_graph_launch()
+ * replays it asynchronously on `stream` (results identical to the eager calls, bit
+ * for bit).  The buffers are baked into the graph: they must stay allocated, and
+ * replays read whatever `in` / `w` hold at launch time.  Errors as conv_forward
+ * (argument checks happen at creation); `*graph_out` is set only on CONV_OK. */
+typedef struct conv_graph_s *conv_graph_t;
+conv_status conv_graph_create(conv_plan_t p, const float *in, const float *w, float *out, void *workspace,
+                              size_t workspace_bytes, int steps, int cached, conv_graph_t *graph_out);
+conv_status conv_graph_launch(conv_graph_t g, void *stream);
+void conv_graph_destroy(conv_graph_t g);   /* NULL-safe */
+
 #ifdef __cplusplus
 }
 #endif

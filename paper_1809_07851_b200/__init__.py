@@ -101,6 +101,9 @@ def load(build_if_missing: bool = False):
         "conv_timer_read": ([vp, fp, ctypes.POINTER(i)], i),
         "conv_timer_reset": ([vp], None),
         "conv_timer_destroy": ([vp], None),
+        "conv_graph_create": ([vp, vp, vp, vp, vp, sz, i, i, ctypes.POINTER(vp)], i),
+        "conv_graph_launch": ([vp, vp], i),
+        "conv_graph_destroy": ([vp], None),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)
@@ -243,6 +246,18 @@ class Plan:
         _check(load().conv_run_stage(self._h, stage, p(x), p(w), p(out), workspace.data_ptr(),
                                      workspace.numel(), _stream_ptr(stream)))
 
+    def capture(self, x, w, out, workspace, steps: int = 1, cached: bool = False) -> "Graph":
+        """conv_graph_create: `steps` forwards on these fixed buffers as one CUDA graph."""
+        _check_tensor(x, "input", self.in_shape)
+        _check_tensor(out, "out", self.out_shape)
+        if not cached:
+            _check_tensor(w, "weights", self.w_shape)
+        h = ctypes.c_void_p()
+        _check(load().conv_graph_create(self._h, x.data_ptr(), 0 if cached else w.data_ptr(), out.data_ptr(),
+                                        workspace.data_ptr(), workspace.numel(), int(steps), int(bool(cached)),
+                                        ctypes.byref(h)))
+        return Graph(h, (self, x, w, out, workspace))
+
     def winograd_matrices(self):
         m, t, r = self.info["m"], self.info["t"], self.info["r"]
         AT = (ctypes.c_double * (m * t))()
@@ -250,6 +265,23 @@ class Plan:
         G = (ctypes.c_double * (t * r))()
         _check(load().conv_plan_winograd_matrices(self._h, AT, BT, G))
         return list(AT), list(BT), list(G)
+
+
+class Graph:
+    """An instantiated CUDA graph of forward passes (conv_graph_*); keeps its buffers alive."""
+
+    def __init__(self, h, keep):
+        self._h = h
+        self._keep = keep
+
+    def launch(self, stream=None):
+        _check(load().conv_graph_launch(self._h, _stream_ptr(stream)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_graph_destroy(h)
+            self._h = None
 
 
 class StageTimer:

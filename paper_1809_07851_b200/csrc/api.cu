@@ -924,4 +924,87 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
     return launch_result(e, "pipelined host forward");
 }
 
+
+// -- CUDA graphs -----------------------------------------------------------------
+struct conv_graph_s {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int device = 0;
+};
+
+void conv_graph_destroy(conv_graph_t gr) {
+    if (!gr) return;
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    if (gr->graph) cudaGraphDestroy(gr->graph);
+    delete gr;
+}
+
+conv_status conv_graph_create(conv_plan_t p, const float *in, const float *w, float *out, void *ws,
+                              size_t ws_bytes, int steps, int cached, conv_graph_t *out_graph) {
+    if (!out_graph || steps < 1) {
+        fc_set_error("NULL graph pointer or steps < 1");
+        return CONV_ERR_INVALID_ARG;
+    }
+    *out_graph = nullptr;
+    conv_status st;
+    if (cached) {
+        if (!p || p->g.method == CONV_DIRECT) {
+            fc_set_error("cached graphs need a fast-method plan");
+            return p ? CONV_ERR_UNSUPPORTED : CONV_ERR_INVALID_ARG;
+        }
+        if ((st = check_device(p))) return st;
+        if ((st = check_dev_ptr(p, in, "in")) || (st = check_dev_ptr(p, out, "out")) ||
+            (st = check_dev_ptr(p, ws, "workspace")))
+            return st;
+        if (ws_bytes < p->ws_bytes) {
+            fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+            return CONV_ERR_INVALID_ARG;
+        }
+    } else if ((st = check_forward_args(p, in, w, out, ws, ws_bytes))) {
+        return st;
+    }
+    conv_graph_s *gr = new (std::nothrow) conv_graph_s();
+    if (!gr) return CONV_ERR_OUT_OF_MEMORY;
+    gr->device = p->device;
+    cudaStream_t cs = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        if (cs) cudaStreamDestroy(cs);
+        delete gr;
+        return launch_result(e, "graph capture begin");
+    }
+    for (int i = 0; i < steps && !st; ++i)
+        st = forward_impl(p, in, w, out, (char *)ws, cs, nullptr, cached != 0);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (st || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        delete gr;
+        return st ? st : launch_result(e, "graph capture end");
+    }
+    gr->graph = graph;
+    e = cudaGraphInstantiate(&gr->exec, graph, 0);
+    if (e != cudaSuccess) {
+        conv_graph_destroy(gr);
+        return launch_result(e, "graph instantiate");
+    }
+    *out_graph = gr;
+    return CONV_OK;
+}
+
+conv_status conv_graph_launch(conv_graph_t gr, void *stream) {
+    if (!gr || !gr->exec) {
+        fc_set_error("NULL graph");
+        return CONV_ERR_INVALID_ARG;
+    }
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != gr->device) {
+        fc_set_error("current device %d != graph device %d", cur, gr->device);
+        return CONV_ERR_DEVICE_MISMATCH;
+    }
+    return launch_result(cudaGraphLaunch(gr->exec, (cudaStream_t)stream), "graph launch");
+}
+
 }  // extern "C"

@@ -339,3 +339,46 @@ def test_plane_pipeline_transforms(name, monkeypatch):
         monkeypatch.delenv("FASTCONV_PLANE")
         assert np.array_equal(y, ref), (name, m)
         assert rel_err(y, O) <= tol("winograd", m, W.shape[2])
+
+
+@pytest.mark.parametrize("method,m", [("winograd", 4), ("regular_fft", 6), ("gauss_fft", 8), ("direct", 0)])
+def test_cuda_graph_forward(method, m):
+    """conv_graph_create / conv_graph_launch: a captured forward (1 and 3 steps per graph)
+    equals the eager conv_forward bit for bit, and a replay picks up new input contents."""
+    cfg = synth.custom(3, 16, 24, 20, 20, 3, seed=101, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    I2, _ = synth.make_inputs(cfg, seed=102)
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m)
+    x, w = I.cuda(), W.cuda()
+    ref = p.forward(x, w).clone()
+    ref2 = p.forward(I2.cuda(), w).clone()
+    ws = p.alloc_workspace()
+    out = torch.full(p.out_shape, float("nan"), device="cuda")
+    for steps in (1, 3):
+        g = p.capture(x, w, out, ws, steps=steps)
+        g.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        x.copy_(I2)
+        g.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref2)
+        x.copy_(I)
+    if method != "direct":  # cached-weights graph
+        wsc = p.alloc_workspace()
+        p.transform_weights(w, wsc)
+        g = p.capture(x, None, out, wsc, cached=True)
+        out.fill_(float("nan"))
+        g.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+
+
+def test_cuda_graph_errors():
+    p = fc.Plan(1, 4, 4, 16, 16, 3, "winograd", 2)
+    lib = fc.load()
+    import ctypes
+    h = ctypes.c_void_p()
+    assert lib.conv_graph_create(p._h, None, None, None, None, 0, 1, 0, ctypes.byref(h)) == 1
+    assert lib.conv_graph_launch(None, None) == 1
+    lib.conv_graph_destroy(None)
