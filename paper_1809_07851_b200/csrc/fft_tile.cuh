@@ -62,17 +62,36 @@ __device__ __forceinline__ void dft_small(cf *x) {
         x[1] = cf{s1.x + r3.x, s1.y + r3.y};
         x[3] = cf{s1.x - r3.x, s1.y - r3.y};
     } else {
+        // odd prime N: pair x_k with x_{N-k} (a_k = sum, b_k = difference), so each output
+        // pair (j, N-j) costs (N-1)/2 real-coefficient complex FMAs on a and on b:
+        //   y_j, y_{N-j} = x_0 + sum_k cos(2 pi jk/N) a_k  +-  i DIR sum_k sin(2 pi jk/N) b_k
+        // (about half the multiplies of the dense O(N^2) complex products)
+        constexpr int Hh = (N - 1) / 2;
+        cf a[Hh], b[Hh];
+        cf y0 = x[0];
+#pragma unroll
+        for (int k = 1; k <= Hh; ++k) {
+            a[k - 1] = cf{x[k].x + x[N - k].x, x[k].y + x[N - k].y};
+            b[k - 1] = cf{x[k].x - x[N - k].x, x[k].y - x[N - k].y};
+            y0.x += a[k - 1].x;
+            y0.y += a[k - 1].y;
+        }
         cf y[N];
+        y[0] = y0;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-            cf acc = x[0];
+        for (int j = 1; j <= Hh; ++j) {
+            cf re = x[0], im{-0.f, -0.f};
 #pragma unroll
-            for (int n = 1; n < N; ++n) {
-                const cf t = twiddle_mul<N, DIR>(x[n], n * k);
-                acc.x += t.x;
-                acc.y += t.y;
+            for (int k = 1; k <= Hh; ++k) {
+                const float2 w = c_tw[tw_base(N) + (j * k) % N];  // (cos, sin)(2 pi jk / N)
+                re.x = fmaf(w.x, a[k - 1].x, re.x);
+                re.y = fmaf(w.x, a[k - 1].y, re.y);
+                im.x = fmaf(w.y, b[k - 1].x, im.x);
+                im.y = fmaf(w.y, b[k - 1].y, im.y);
             }
-            y[k] = acc;
+            const cf t = DIR > 0 ? cf{-im.y, im.x} : cf{im.y, -im.x};  // i * DIR * im
+            y[j] = cf{re.x + t.x, re.y + t.y};
+            y[N - j] = cf{re.x - t.x, re.y - t.y};
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) x[k] = y[k];
