@@ -179,6 +179,28 @@ def cpu_baseline(cfg, seconds: float):
                       % (nb, cfg.B, co, cfg.Cout, cfg.name, flops / cfg.direct_flops, dt)}
 
 
+def cpu_direct_baseline(cfg, seconds: float):
+    """The straightforward multithreaded fp32 CPU direct convolution (cpu_baseline/) on a
+    bounded sample of the workload: the first n images, all output channels."""
+    import cpu_baseline
+    import synth
+    I, W = synth.make_inputs(cfg)
+    cpu_baseline.conv_fp32(I[:1].contiguous(), W[:8].contiguous())  # warm the OpenMP pool
+    t = time.perf_counter()
+    cpu_baseline.conv_fp32(I[:1].contiguous(), W)
+    per_img = max(time.perf_counter() - t, 1e-5)
+    nb = int(max(1, min(cfg.B, seconds / per_img)))
+    Is = I[:nb].contiguous()
+    t = time.perf_counter()
+    cpu_baseline.conv_fp32(Is, W)
+    dt = time.perf_counter() - t
+    flops = 2.0 * nb * cfg.C * cfg.Cout * cfg.Ho * cfg.Wo * cfg.r * cfg.r
+    return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cpu_baseline.num_threads(),
+            "kind": "direct_fp32 (OpenMP over (b, c'), -O3 -march=native, no blocking)",
+            "sample": "%d of %d images x all %d output channels of %s (%.3g of the layer's direct FLOPs), %.1f s"
+                      % (nb, cfg.B, cfg.Cout, cfg.name, flops / cfg.direct_flops, dt)}
+
+
 # ------------------------------------------------------------------- main ---
 def main():
     ap = argparse.ArgumentParser()
@@ -407,9 +429,10 @@ def main():
                "h2d_bytes_per_step": I.numel() * 4 + W.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
                "api": "conv_forward_host (pinned host in/w/out; H2D, kernels and D2H pipelined over 8 image chunks)"}
 
-    cpu = None
+    cpu = cpu_fp32 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_baseline_s)
+        cpu_fp32 = cpu_direct_baseline(cfg, args.cpu_baseline_s)
 
     if rank == 0:
         line = {
@@ -434,6 +457,7 @@ def main():
             "inference_cached_weights": cached,
             "cuda_graph": graph,
             "cpu_baseline": cpu,
+            "cpu_direct_fp32": cpu_fp32,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": plan.launches * args.steps,
