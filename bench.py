@@ -196,7 +196,7 @@ def cpu_direct_baseline(cfg, seconds: float):
     dt = time.perf_counter() - t
     flops = 2.0 * nb * cfg.C * cfg.Cout * cfg.Ho * cfg.Wo * cfg.r * cfg.r
     return {"value": flops / dt / 1e12, "unit": UNIT, "cores": cpu_baseline.num_threads(),
-            "kind": "direct_fp32 (OpenMP over (b, c'), -O3 -march=native, no blocking)",
+            "kind": "direct_fp32 (OpenMP over (b, c'), -O3 -mavx2 -mfma, no blocking)",
             "sample": "%d of %d images x all %d output channels of %s (%.3g of the layer's direct FLOPs), %.1f s"
                       % (nb, cfg.B, cfg.Cout, cfg.name, flops / cfg.direct_flops, dt)}
 

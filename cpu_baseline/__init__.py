@@ -18,7 +18,8 @@ _lib = None
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O3", "-march=native", "-fopenmp", "-shared", "-fPIC", "-o", _LIB + ".tmp", _SRC]
+        # AVX2 + FMA (not -march=native: the .so built here also runs on the GPU box's host CPU)
+        cmd = ["gcc", "-O3", "-mavx2", "-mfma", "-fopenmp", "-shared", "-fPIC", "-o", _LIB + ".tmp", _SRC]
         subprocess.run(cmd, check=True)
         os.replace(_LIB + ".tmp", _LIB)
     return _LIB

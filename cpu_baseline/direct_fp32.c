@@ -3,7 +3,7 @@
  *
  * The "straightforward multithreaded CPU direct conv" of BASELINE.json's north_star:
  * fp32 arithmetic, OpenMP over (b, c') output planes, the output row innermost so
- * the compiler vectorises along j (-O3 -march=native), no blocking or packing
+ * the compiler vectorises along j (-O3 -mavx2 -mfma), no blocking or packing
  * tricks.  Same problem statement as the product path (Eq. 5,
  * valid cross-correlation, W[c'][c][p][q]; readings R1-R3).  It is not
  * the parity oracle (oracle/ is fp64) and shares no code with either.
