@@ -262,6 +262,40 @@ __device__ __forceinline__ void store_strip(float *__restrict__ dst, const float
     }
 }
 
+// r[q] = sum_l A^T[q][l] x[l] for the compile-time A^T of F(MM, T-MM+1).  The finite
+// points are ordered 0, 1, -1, 2, -2, 1/2, -1/2 (wtab::point), so columns (2j+1, 2j+2)
+// hold +-p and A^T[q][2j+2] = (-1)^q A^T[q][2j+1]: each pair costs one sum and one
+// difference shared by all rows (checked at compile time by at_pairs_ok).
+template <int T, int MM>
+__host__ __device__ constexpr bool at_pairs_ok() {
+    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);
+    for (int q = 0; q < MM; ++q)
+        for (int j = 0; 2 * j + 2 <= T - 2; ++j)
+            if (ta.AT[q][2 * j + 2] != ((q & 1) ? -ta.AT[q][2 * j + 1] : ta.AT[q][2 * j + 1])) return false;
+    return true;
+}
+
+template <int T, int MM>
+__device__ __forceinline__ void at_rows(const float *x, float *r) {
+    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);
+    static_assert(at_pairs_ok<T, MM>(), "A^T columns are not +-p pairs");
+    constexpr int NP = (T - 2) / 2;
+    float sp[NP > 0 ? NP : 1], dp[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+        sp[j] = x[2 * j + 1] + x[2 * j + 2];
+        dp[j] = x[2 * j + 1] - x[2 * j + 2];
+    }
+#pragma unroll
+    for (int q = 0; q < MM; ++q) {
+        float acc = wtab::cfma(ta.AT[q][0], x[0], -0.f);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc = wtab::cfma(ta.AT[q][2 * j + 1], (q & 1) ? dp[j] : sp[j], acc);
+        if ((T - 2) & 1) acc = wtab::cfma(ta.AT[q][T - 2], x[T - 2], acc);
+        r[q] = wtab::cfma(ta.AT[q][T - 1], x[T - 1], acc);
+    }
+}
+
 // ----------------------------------------------------------- Winograd NK4 ---
 // CTA = (strip of R tile rows, output channel c', image b).  One thread per tile
 // loads its t^2 elements of X along n, computes Y = A^T X A, and writes the m x m
@@ -292,23 +326,54 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
 #pragma unroll
             for (int q = 0; q < MM; ++q) y[a][q] = -0.f;
         const float *sp = src0 + tl;
+        // rows of X in the order 0, (1,2), (3,4), ..., [T-2], T-1: a +-p row pair enters Y as
+        // its sum (even output rows a) or difference (odd a), as the columns do in at_rows
+        auto load_row = [&](int k, float *x) {
 #pragma unroll
-        for (int k = 0; k < T; ++k) {
-            float x[T];
+            for (int l = 0; l < T; ++l) x[l] = __ldcs(sp + (size_t)(k * T + l) * estride);
+        };
+        auto add_row = [&](int k, const float *r) {
 #pragma unroll
-            for (int l = 0; l < T; ++l) {
-                x[l] = __ldcs(sp);
-                sp += estride;
-            }
-            if (k & 1) asm volatile("" ::: "memory");  // keep ~2 rows of loads in flight, not all t^2
+            for (int a = 0; a < MM; ++a)
+#pragma unroll
+                for (int q = 0; q < MM; ++q) y[a][q] = wtab::cfma(ta.AT[a][k], r[q], y[a][q]);
+        };
+        {
+            float x[T], r[MM];
+            load_row(0, x);
+            at_rows<T, MM>(x, r);
+            add_row(0, r);
+        }
+#pragma unroll
+        for (int j = 0; 2 * j + 2 <= T - 2; ++j) {
+            float x1[T], x2[T], r1[MM], r2[MM], rs[MM], rd[MM];
+            load_row(2 * j + 1, x1);
+            load_row(2 * j + 2, x2);
+            at_rows<T, MM>(x1, r1);
+            at_rows<T, MM>(x2, r2);
 #pragma unroll
             for (int q = 0; q < MM; ++q) {
-                float rq = -0.f;
-#pragma unroll
-                for (int l = 0; l < T; ++l) rq = wtab::cfma(ta.AT[q][l], x[l], rq);
-#pragma unroll
-                for (int a = 0; a < MM; ++a) y[a][q] = wtab::cfma(ta.AT[a][k], rq, y[a][q]);
+                rs[q] = r1[q] + r2[q];
+                rd[q] = r1[q] - r2[q];
             }
+#pragma unroll
+            for (int a = 0; a < MM; ++a)
+#pragma unroll
+                for (int q = 0; q < MM; ++q)
+                    y[a][q] = wtab::cfma(ta.AT[a][2 * j + 1], (a & 1) ? rd[q] : rs[q], y[a][q]);
+            asm volatile("" ::: "memory");  // keep about one row pair of loads in flight
+        }
+        if ((T - 2) & 1) {
+            float x[T], r[MM];
+            load_row(T - 2, x);
+            at_rows<T, MM>(x, r);
+            add_row(T - 2, r);
+        }
+        {
+            float x[T], r[MM];
+            load_row(T - 1, x);
+            at_rows<T, MM>(x, r);
+            add_row(T - 1, r);
         }
         const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
         float *q0 = so + ti * m * SWo + tj * m;
