@@ -173,75 +173,6 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
 }
 
 
-// Two horizontally adjacent tiles per thread (even n_w): the 2-tile window
-// (m + t columns) is read with 8-byte vector loads (x0 = 2pm is even) and the
-// two results of every transformed element are written as one float2 at
-// (n, n+1) -- half the load/store instructions of one tile per thread.
-template <int T, int MM>
-__global__ void __launch_bounds__(128) nk2_wino_pair(Geometry g, const float *__restrict__ in,
-                                                     float *__restrict__ U) {
-    constexpr wtab::Tables tb = wtab::make(2, T - 1);
-    constexpr int WID = MM + T;  // columns covered by the two tiles
-    const long long pidx = (long long)blockIdx.x * 128 + threadIdx.x;
-    const int c = blockIdx.y;
-    const bool valid = 2 * pidx < g.BN;
-    const long long n = valid ? 2 * pidx : 0;
-    const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
-    const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
-    const int y0 = ti * MM, x0 = tj * MM;
-    const float *src = in + ((size_t)b * g.C + c) * g.H * g.W + (size_t)y0 * g.W + x0;
-    const bool interior = (y0 + T <= g.H) && (x0 + WID <= g.W);
-    const bool vec = interior && ((g.W & 1) == 0);
-    float zA[T][T], zB[T][T];
-#pragma unroll
-    for (int a = 0; a < T; ++a) {
-        float d[WID];
-        if (vec) {
-            const float2 *r2 = reinterpret_cast<const float2 *>(src + a * g.W);
-#pragma unroll
-            for (int q = 0; q < WID / 2; ++q) {
-                const float2 v = __ldg(r2 + q);
-                d[2 * q] = v.x;
-                d[2 * q + 1] = v.y;
-            }
-            if (WID & 1) d[WID - 1] = __ldg(src + a * g.W + WID - 1);
-        } else {
-#pragma unroll
-            for (int q = 0; q < WID; ++q)
-                d[q] = (y0 + a < g.H && x0 + q < g.W) ? __ldg(src + a * g.W + q) : 0.f;
-        }
-#pragma unroll
-        for (int l = 0; l < T; ++l) {
-            float sa = -0.f, sb = -0.f;
-#pragma unroll
-            for (int q = 0; q < T; ++q) {
-                sa = wtab::cfma(tb.BT[l][q], d[q], sa);
-                sb = wtab::cfma(tb.BT[l][q], d[MM + q], sb);
-            }
-            zA[a][l] = sa;
-            zB[a][l] = sb;
-        }
-    }
-    const size_t estride = (size_t)g.K * g.BN_pad;
-    float *dp = U + (size_t)c * g.BN_pad + n;
-    float umx = 0.f;
-#pragma unroll
-    for (int k = 0; k < T; ++k)
-#pragma unroll
-        for (int l = 0; l < T; ++l) {
-            float sa = -0.f, sb = -0.f;
-#pragma unroll
-            for (int a = 0; a < T; ++a) {
-                sa = wtab::cfma(tb.BT[k][a], zA[a][l], sa);
-                sb = wtab::cfma(tb.BT[k][a], zB[a][l], sb);
-            }
-            if (valid) *reinterpret_cast<float2 *>(dp) = make_float2(sa, sb);
-            umx = fmaxf(umx, fmaxf(fabsf(sa), fabsf(sb)));
-            dp += estride;
-        }
-    if (g.umax) fc_block_umax(g.umax, umx);
-}
-
 // Copy `rows` staged output rows (pitch SWo floats in smem) to `rows` contiguous rows
 // of Wo floats in global memory: one warp per row, lanes along the row (coalesced,
 // streaming stores, no per-element division).
@@ -1073,11 +1004,7 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
     cudaError_t perr = cudaSuccess;
     if (launch_wino_plane<T, MM>(g, src, dst, forward, s, &perr)) return perr;
     if (forward) {
-        static const int no_pair = getenv("FASTCONV_NK2_PAIR") == nullptr;
-        if (g.n_w % 2 == 0 && !no_pair) {
-            const unsigned nblk = (unsigned)((g.BN / 2 + 127) / 128);
-            nk2_wino_pair<T, MM><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
-        } else {
+        {
             static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
             if (g.umax) {
                 const unsigned nblk = (unsigned)((g.BN + 127) / 128);
