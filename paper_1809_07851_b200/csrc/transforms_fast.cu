@@ -227,6 +227,61 @@ __device__ __forceinline__ void at_rows(const float *x, float *r) {
     }
 }
 
+// Y = A^T X A for one tile, X streamed by rows through load_row(k, x[T]) in the order
+// 0, (1,2), (3,4), ..., [T-2], T-1: a +-p row pair enters Y as its sum (even output
+// rows a) or difference (odd a), as the columns do in at_rows.  Shared by both NK4
+// kernels so their results are bit-identical.
+template <int T, int MM, typename LoadRow>
+__device__ __forceinline__ void wino_out_tile(LoadRow load_row, float (&y)[MM][MM]) {
+    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);
+#pragma unroll
+    for (int a = 0; a < MM; ++a)
+#pragma unroll
+        for (int q = 0; q < MM; ++q) y[a][q] = -0.f;
+    auto add_row = [&](int k, const float *r) {
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int q = 0; q < MM; ++q) y[a][q] = wtab::cfma(ta.AT[a][k], r[q], y[a][q]);
+    };
+    {
+        float x[T], r[MM];
+        load_row(0, x);
+        at_rows<T, MM>(x, r);
+        add_row(0, r);
+    }
+#pragma unroll
+    for (int j = 0; 2 * j + 2 <= T - 2; ++j) {
+        float x1[T], x2[T], r1[MM], r2[MM], rs[MM], rd[MM];
+        load_row(2 * j + 1, x1);
+        load_row(2 * j + 2, x2);
+        at_rows<T, MM>(x1, r1);
+        at_rows<T, MM>(x2, r2);
+#pragma unroll
+        for (int q = 0; q < MM; ++q) {
+            rs[q] = r1[q] + r2[q];
+            rd[q] = r1[q] - r2[q];
+        }
+#pragma unroll
+        for (int a = 0; a < MM; ++a)
+#pragma unroll
+            for (int q = 0; q < MM; ++q) y[a][q] = wtab::cfma(ta.AT[a][2 * j + 1], (a & 1) ? rd[q] : rs[q], y[a][q]);
+        asm volatile("" ::: "memory");  // keep about one row pair of loads in flight
+    }
+    if ((T - 2) & 1) {
+        float x[T], r[MM];
+        load_row(T - 2, x);
+        at_rows<T, MM>(x, r);
+        add_row(T - 2, r);
+    }
+    {
+        float x[T], r[MM];
+        load_row(T - 1, x);
+        at_rows<T, MM>(x, r);
+        add_row(T - 1, r);
+    }
+}
+
 // ----------------------------------------------------------- Winograd NK4 ---
 // CTA = (strip of R tile rows, output channel c', image b).  One thread per tile
 // loads its t^2 elements of X along n, computes Y = A^T X A, and writes the m x m
@@ -249,63 +304,15 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     const size_t estride = (size_t)g.M * g.BN_pad;
     const float *src0 = X + (size_t)co * g.BN_pad + nbase;
     for (int tl = threadIdx.x; tl < ntiles; tl += blockDim.x) {
-        // stream the tile row by row: r_k = X[k][:] A (m values), Y += A^T[:, k] r_k,
-        // so only one row of X and the m x m accumulator are live (registers / occupancy)
+        // stream the tile by rows of X (one row pair live at a time: registers / occupancy)
         float y[MM][MM];
-#pragma unroll
-        for (int a = 0; a < MM; ++a)
-#pragma unroll
-            for (int q = 0; q < MM; ++q) y[a][q] = -0.f;
         const float *sp = src0 + tl;
-        // rows of X in the order 0, (1,2), (3,4), ..., [T-2], T-1: a +-p row pair enters Y as
-        // its sum (even output rows a) or difference (odd a), as the columns do in at_rows
-        auto load_row = [&](int k, float *x) {
+        wino_out_tile<T, MM>(
+            [&](int k, float *x) {
 #pragma unroll
-            for (int l = 0; l < T; ++l) x[l] = __ldcs(sp + (size_t)(k * T + l) * estride);
-        };
-        auto add_row = [&](int k, const float *r) {
-#pragma unroll
-            for (int a = 0; a < MM; ++a)
-#pragma unroll
-                for (int q = 0; q < MM; ++q) y[a][q] = wtab::cfma(ta.AT[a][k], r[q], y[a][q]);
-        };
-        {
-            float x[T], r[MM];
-            load_row(0, x);
-            at_rows<T, MM>(x, r);
-            add_row(0, r);
-        }
-#pragma unroll
-        for (int j = 0; 2 * j + 2 <= T - 2; ++j) {
-            float x1[T], x2[T], r1[MM], r2[MM], rs[MM], rd[MM];
-            load_row(2 * j + 1, x1);
-            load_row(2 * j + 2, x2);
-            at_rows<T, MM>(x1, r1);
-            at_rows<T, MM>(x2, r2);
-#pragma unroll
-            for (int q = 0; q < MM; ++q) {
-                rs[q] = r1[q] + r2[q];
-                rd[q] = r1[q] - r2[q];
-            }
-#pragma unroll
-            for (int a = 0; a < MM; ++a)
-#pragma unroll
-                for (int q = 0; q < MM; ++q)
-                    y[a][q] = wtab::cfma(ta.AT[a][2 * j + 1], (a & 1) ? rd[q] : rs[q], y[a][q]);
-            asm volatile("" ::: "memory");  // keep about one row pair of loads in flight
-        }
-        if ((T - 2) & 1) {
-            float x[T], r[MM];
-            load_row(T - 2, x);
-            at_rows<T, MM>(x, r);
-            add_row(T - 2, r);
-        }
-        {
-            float x[T], r[MM];
-            load_row(T - 1, x);
-            at_rows<T, MM>(x, r);
-            add_row(T - 1, r);
-        }
+                for (int l = 0; l < T; ++l) x[l] = __ldcs(sp + (size_t)(k * T + l) * estride);
+            },
+            y);
         const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
         float *q0 = so + ti * m * SWo + tj * m;
 #pragma unroll
@@ -869,24 +876,12 @@ __global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *_
         for (int it = threadIdx.x; it < ng * g.N; it += blockDim.x) {
             const int gi = it / g.N, tile = it - gi * g.N;
             float y[MM][MM];
+            wino_out_tile<T, MM>(
+                [&](int k, float *x) {
 #pragma unroll
-            for (int a = 0; a < MM; ++a)
-#pragma unroll
-                for (int qq = 0; qq < MM; ++qq) y[a][qq] = -0.f;
-#pragma unroll
-            for (int kk = 0; kk < T; ++kk) {
-                float x[T];
-#pragma unroll
-                for (int l = 0; l < T; ++l) x[l] = sp[(kk * T + l) * GN + it];
-#pragma unroll
-                for (int qq = 0; qq < MM; ++qq) {
-                    float rq = -0.f;
-#pragma unroll
-                    for (int l = 0; l < T; ++l) rq = wtab::cfma(ta.AT[qq][l], x[l], rq);
-#pragma unroll
-                    for (int a = 0; a < MM; ++a) y[a][qq] = wtab::cfma(ta.AT[a][kk], rq, y[a][qq]);
-                }
-            }
+                    for (int l = 0; l < T; ++l) x[l] = sp[(k * T + l) * GN + it];
+                },
+                y);
             const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
             const int oy = ti * MM, ox = tj * MM;
             float *op = out + (((size_t)(b0 + gi) * g.Cout + co) * g.Ho + oy) * g.Wo + ox;
