@@ -178,6 +178,17 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
 // streaming stores, no per-element division).
 __device__ __forceinline__ void store_strip(float *__restrict__ dst, const float *__restrict__ src, int rows, int Wo,
                                             int SWo) {
+    if (SWo == Wo && ((((uintptr_t)dst) | ((uintptr_t)src)) & 15) == 0 && (Wo & 3) == 0) {
+        // the staged rows have the output's pitch: one flat run of 16-byte vectors
+        const float4 *s4 = reinterpret_cast<const float4 *>(src);
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        for (int i = threadIdx.x; i < (rows * Wo) >> 2; i += blockDim.x) __stcs(d4 + i, s4[i]);
+        return;
+    }
+    if (SWo == Wo) {  // same pitch, unaligned: one flat scalar run
+        for (int i = threadIdx.x; i < rows * Wo; i += blockDim.x) __stcs(dst + i, src[i]);
+        return;
+    }
     if (Wo < 48) {  // narrow rows: flat index (one division per element) keeps every lane busy
         for (int idx = threadIdx.x; idx < rows * Wo; idx += blockDim.x) {
             const int r = idx / Wo, c = idx - r * Wo;
@@ -338,11 +349,7 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     for (int im = 0; im < nimg; ++im) {
         float *dst = out + (((size_t)(b + im) * g.Cout + co) * g.Ho + y0) * g.Wo;
         const float *src = so + (size_t)im * ntr * m * SWo;
-        if (SWo == g.Wo) {
-            for (int idx = threadIdx.x; idx < orows * g.Wo; idx += blockDim.x) __stcs(dst + idx, src[idx]);
-        } else {
-            store_strip(dst, src, orows, g.Wo, SWo);
-        }
+        store_strip(dst, src, orows, g.Wo, SWo);
     }
 }
 
