@@ -16,6 +16,9 @@
 
 #include <new>
 
+#include <mutex>
+#include <set>
+
 #include "common.h"
 
 static thread_local char g_err[512] = "";
@@ -153,6 +156,26 @@ conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G
 // Geometry + algorithmic cost
 // ---------------------------------------------------------------------------
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+cudaError_t fc_smem_attr(const void *func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({func, dev});
+    return e;
+}
+
+int fc_num_sms() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return 148;
+    return n;
+}
 
 Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
     Geometry c = g;

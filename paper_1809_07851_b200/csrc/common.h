@@ -171,7 +171,13 @@ __device__ __forceinline__ float fc_pow2_scale(float mx, int top) {
 // geometry of a chunk of Bc images (U / X row pitch BN_pad follows the chunk)
 Geometry fc_chunk_geometry(const Geometry &g, int Bc);
 
-// ---- host helpers (plan.cu) ----
+// ---- host helpers ----
+// Allow `bytes` of dynamic shared memory for `func` on the current device, once per
+// (kernel, device): the attribute is per device, so a process that drives several
+// GPUs sets it on each (thread-safe).
+cudaError_t fc_smem_attr(const void *func, int bytes);
+// SM count of the current device (persistent grids)
+int fc_num_sms();
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
                              Geometry *g, conv_plan_info *info, conv_gemm_impl gemm);
 conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G);

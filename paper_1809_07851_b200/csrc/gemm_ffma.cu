@@ -115,11 +115,7 @@ cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w,
     const int P = DT + g.r - 1;
     const size_t smem = sizeof(float) * ((size_t)P * P + (size_t)DCO * g.r * g.r);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(nk5_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    fc_smem_attr((const void *)nk5_direct, 200 * 1024);
     const int tiles = ((g.Ho + DT - 1) / DT) * ((g.Wo + DT - 1) / DT);
     dim3 grid((unsigned)tiles, (unsigned)((g.Cout + DCO - 1) / DCO), (unsigned)g.B);
     nk5_direct<<<grid, 256, smem, s>>>(g, in, w, out);

@@ -758,7 +758,6 @@ bool encode_3d(CUtensorMap *map, const void *ptr, uint64_t d0, uint64_t d1, uint
     return r == CUDA_SUCCESS;
 }
 
-int g_num_sms = 0;
 
 template <int CG, int BLOCK_N, int STAGES, int BK>
 cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
@@ -778,17 +777,11 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     auto kern = nk3_gemm_tcgen05<CG, BLOCK_N, STAGES, BK>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    {
+        cudaError_t e = fc_smem_attr((const void *)kern, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        configured = true;
     }
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int g_num_sms = fc_num_sms();
     const long long n_m = (g.M + Cfg::BM - 1) / Cfg::BM;
     const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
     const long long tiles = (long long)g.Z * n_m * n_n;
@@ -833,17 +826,11 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, SA, SU>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    {
+        cudaError_t e = fc_smem_attr((const void *)kern, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        configured = true;
     }
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int g_num_sms = fc_num_sms();
     const long long n_m = (g.M + Cfg::BM - 1) / Cfg::BM;
     const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
     const long long tiles = (long long)g.Z * n_m * n_n;

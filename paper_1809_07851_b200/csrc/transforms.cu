@@ -356,11 +356,7 @@ cudaError_t fc_launch_input_transform(const Geometry &g, const ConvConsts *dc, c
     const bool fft = g.method != CONV_WINOGRAD;
     const size_t smem = sizeof(float) * (2 * FC_MAX_T + (size_t)TN * g.t * g.t +
                                          (size_t)TN * g.t * (fft ? 2 * g.h : g.t));
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(nk2_input_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    fc_smem_attr((const void *)nk2_input_transform, 200 * 1024);
     dim3 grid((unsigned)((g.BN + TN - 1) / TN), (unsigned)g.C);
     nk2_input_transform<<<grid, 256, smem, s>>>(g, dc, in, U, TN);
     return cudaGetLastError();
@@ -373,11 +369,7 @@ cudaError_t fc_launch_output_transform(const Geometry &g, const ConvConsts *dc, 
     const int cw = fft ? 2 : 1;
     const size_t smem = sizeof(float) * (2 * FC_MAX_T + (size_t)TN * g.E * cw +
                                          (size_t)TN * g.m * (fft ? g.h : g.t) * cw);
-    static int configured = 0;
-    if (!configured) {
-        cudaFuncSetAttribute(nk4_output_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 1;
-    }
+    fc_smem_attr((const void *)nk4_output_transform, 200 * 1024);
     dim3 grid((unsigned)((g.BN + TN - 1) / TN), (unsigned)g.Cout);
     nk4_output_transform<<<grid, 256, smem, s>>>(g, dc, X, out, TN);
     return cudaGetLastError();

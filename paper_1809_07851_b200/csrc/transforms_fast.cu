@@ -669,11 +669,7 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
     const unsigned nblk = (unsigned)((g.BN + FTN - 1) / FTN);
     if (forward) {
         const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(nk2_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cfg = true;
-        }
+        fc_smem_attr((const void *)nk2_fft<T>, (int)smem);
         nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst);
     } else {
         // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
@@ -695,11 +691,7 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         while (R > 1 && smem_of(IPC, R) > 100 * 1024) --R;
         const size_t smem = smem_of(IPC, R);
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(nk4_fft<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cfg = true;
-        }
+        fc_smem_attr((const void *)nk4_fft<T>, 200 * 1024);
         const int nstrip = (g.n_h + R - 1) / R;
         const int ngroup = (g.B + IPC - 1) / IPC;
         const int items = H * IPC * R * g.n_w;
@@ -924,15 +916,7 @@ __global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *_
     }
 }
 
-int g_sms_tf = 0;
-int sm_count() {
-    if (!g_sms_tf) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms_tf, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return g_sms_tf;
-}
+int sm_count() { return fc_num_sms(); }
 
 // plane-pipeline launchers: return false when the geometry does not qualify
 template <int T, int MM>
@@ -954,18 +938,10 @@ bool launch_wino_plane(const Geometry &g, const float *src, float *dst, bool for
         long long grid = (long long)sm_count() * (per_sm < 1 ? 1 : per_sm);
         if (grid > total) grid = total;
         if (g.umax) {
-            static bool cfg = false;
-            if (!cfg) {
-                cudaFuncSetAttribute(nk2_wino_plane<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cfg = true;
-            }
+            fc_smem_attr((const void *)nk2_wino_plane<T, true>, 200 * 1024);
             nk2_wino_plane<T, true><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
         } else {
-            static bool cfg = false;
-            if (!cfg) {
-                cudaFuncSetAttribute(nk2_wino_plane<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-                cfg = true;
-            }
+            fc_smem_attr((const void *)nk2_wino_plane<T, false>, 200 * 1024);
             nk2_wino_plane<T, false><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
         }
     } else {
@@ -980,11 +956,7 @@ bool launch_wino_plane(const Geometry &g, const float *src, float *dst, bool for
         const long long total = (long long)g.Cout * ((g.B + G - 1) / G);
         long long grid = (long long)sm_count() * per_sm;
         if (grid > total) grid = total;
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(nk4_wino_plane<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cfg = true;
-        }
+        fc_smem_attr((const void *)nk4_wino_plane<T, MM>, 200 * 1024);
         nk4_wino_plane<T, MM><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
     }
     *err = cudaGetLastError();
@@ -1032,11 +1004,7 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
         const int ngroup = (g.B + IPC - 1) / IPC;
         const size_t smem = sizeof(float) * (size_t)IPC * R * g.m * SWo;
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(nk4_wino<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            cfg = true;
-        }
+        fc_smem_attr((const void *)nk4_wino<T, MM>, 200 * 1024);
         const int tiles = IPC * R * g.n_w;
         const int threads = tiles >= 256 ? 256 : (tiles + 31) / 32 * 32;
         nk4_wino<T, MM><<<dim3(nstrip * ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
