@@ -115,7 +115,8 @@ typedef struct {
 conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r,
                             conv_method method, int m, conv_plan_info *info);
 
-/* Create a plan on the current CUDA device (uploads ~KB of constants:
+/* Create a plan on the current CUDA device, which must be sm_100 (B200; the library
+ * carries sm_100a code only -- other devices get CONV_ERR_UNSUPPORTED) (uploads ~KB of constants:
  * Winograd matrices built exactly in rationals, DFT twiddles computed in fp64,
  * both rounded once to fp32).  m is ignored for CONV_DIRECT.  `*out` is set
  * only on CONV_OK; release with conv_destroy. */

@@ -426,6 +426,16 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
         free(p);
         return CONV_ERR_CUDA;
     }
+    {  // the library carries sm_100a code only (no PTX): refuse other devices up front
+        int major = 0, minor = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, p->device);
+        if (major != 10 || minor != 0) {
+            fc_set_error("device %d is sm_%d%d; this build targets sm_100a (B200) only", p->device, major, minor);
+            free(p);
+            return CONV_ERR_UNSUPPORTED;
+        }
+    }
     if (method != CONV_DIRECT) {
         if (method != CONV_WINOGRAD && (e = fc_init_twiddles()) != cudaSuccess) {
             fc_set_error("twiddle upload: %s", cudaGetErrorString(e));
