@@ -181,7 +181,7 @@ Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
     Geometry c = g;
     c.B = Bc;
     c.BN = (long long)Bc * g.N;
-    c.BN_pad = (c.BN + 31) / 32 * 32;
+    c.BN_pad = (c.BN + FC_TB - 1) / FC_TB * FC_TB;
     return c;
 }
 
@@ -276,7 +276,7 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         G.N = G.n_h * G.n_w;
         G.E = G.t * G.h;
         G.BN = (long long)B * G.N;
-        G.BN_pad = (G.BN + 31) / 32 * 32;
+        G.BN_pad = (G.BN + FC_TB - 1) / FC_TB * FC_TB;
         if (method == CONV_REGULAR_FFT) {  // real embedding of the complex product
             G.Z = G.E; G.M = 2 * Cout; G.K = 2 * C;
         } else if (method == CONV_GAUSS_FFT) {

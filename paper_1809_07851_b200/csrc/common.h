@@ -60,6 +60,16 @@ struct conv_plan_s {
     conv_plan_info info;
 };
 
+// U layout, blocked by FC_TB tiles: U[nb][k][z][t] with n = nb * FC_TB + t, so one
+// NK2 CTA's (channel, 128 tiles) output is a single contiguous run of Z * 512 bytes
+// and consecutive transformed elements z sit 512 bytes apart (store immediates); the
+// contraction reads (128 tiles x 32 k) boxes of one (z, nb) with a 4-D tensor map.
+// BN_pad is a multiple of FC_TB.
+#define FC_TB 128
+inline __host__ __device__ size_t fc_u_off(const Geometry &g, long long n, int k, int z) {
+    return (((size_t)(n / FC_TB) * g.K + k) * g.Z + z) * FC_TB + (size_t)(n % FC_TB);
+}
+
 // elements of V (one of V_hi / V_lo; fp32, or fp16 in F16X3 mode)
 inline size_t fc_v_floats(const Geometry &g) {
     return g.cplx ? (size_t)2 * g.E * g.Cout * g.Kp : (size_t)g.Z * g.M * g.Kp;

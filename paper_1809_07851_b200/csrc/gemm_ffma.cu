@@ -12,14 +12,14 @@ namespace {
 constexpr int BM = 64, BNT = 64, BK = 16;
 
 __global__ void __launch_bounds__(256) nk3_gemm_ffma(const float *__restrict__ A, const float *__restrict__ Bm,
-                                                     float *__restrict__ X, int M, int K, int lda, long long NP) {
+                                                     float *__restrict__ X, int M, int K, int lda, long long NP,
+                                                     int Zn) {
     __shared__ float As[BK][BM + 4];
     __shared__ __align__(16) float Bs[BK][BNT];
     const int z = blockIdx.z;
     const int m0 = blockIdx.y * BM;
     const long long n0 = (long long)blockIdx.x * BNT;
     const float *Az = A + (size_t)z * M * lda;
-    const float *Bz = Bm + (size_t)z * K * NP;
     float *Xz = X + (size_t)z * M * NP;
     const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
     float acc[4][4] = {};
@@ -33,7 +33,10 @@ __global__ void __launch_bounds__(256) nk3_gemm_ffma(const float *__restrict__ A
             const int kk = i / BNT, col = i % BNT;
             const int gk = k0 + kk;
             const long long gn = n0 + col;
-            Bs[kk][col] = (gk < K && gn < NP) ? Bz[(size_t)gk * NP + gn] : 0.f;
+            // U blocked by FC_TB tiles: U[n / TB][k][z][n % TB]
+            Bs[kk][col] = (gk < K && gn < NP)
+                              ? Bm[(((size_t)(gn / FC_TB) * K + gk) * Zn + z) * FC_TB + (size_t)(gn % FC_TB)]
+                              : 0.f;
         }
         __syncthreads();
 #pragma unroll
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(256) nk5_direct(Geometry g, const float *__res
 
 cudaError_t fc_launch_gemm_ffma(const Geometry &g, const float *V, const float *U, float *X, cudaStream_t s) {
     dim3 grid((unsigned)((g.BN_pad + BNT - 1) / BNT), (unsigned)((g.M + BM - 1) / BM), (unsigned)g.Z);
-    nk3_gemm_ffma<<<grid, 256, 0, s>>>(V, U, X, g.M, g.K, g.Kp, g.BN_pad);
+    nk3_gemm_ffma<<<grid, 256, 0, s>>>(V, U, X, g.M, g.K, g.Kp, g.BN_pad, g.Z);
     return cudaGetLastError();
 }
 

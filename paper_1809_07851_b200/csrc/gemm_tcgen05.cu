@@ -66,6 +66,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
         "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+            dst),
+        "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -274,9 +282,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tma_load_3d(sA, &tmA, full_bar(stage), ak, ar, az);
                     tma_load_3d(sAlo, &tmAlo, full_bar(stage), ak, ar, az);
 #pragma unroll
-                    for (int j = 0; j < Cfg::NH / 32; ++j)
-                        tma_load_3d(sB + j * (BK * 128), &tmB, full_bar(stage), n0 + (int)rank * Cfg::NH + 32 * j,
-                                    kb * BK, z);
+                    for (int j = 0; j < Cfg::NH / 32; ++j) {  // U blocked by FC_TB tiles: (t, z, k, block)
+                        const int nc = n0 + (int)rank * Cfg::NH + 32 * j;
+                        tma_load_4d(sB + j * (BK * 128), &tmB, full_bar(stage), nc % FC_TB, z, kb * BK, nc / FC_TB);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -538,8 +547,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < num_k; ++kb) {
                     mbar_wait(emptyU_bar(su), pu ^ 1);
                     mbar_expect_tx(fullU_bar(su), Cfg::UF_BYTES);
-                    tma_load_3d(ubase + su * Cfg::UF_BYTES, &tmU, fullU_bar(su), n0 + (int)rank * Cfg::NH,
-                                kb * BK, z);
+                    {  // U blocked by FC_TB tiles: box (NH tiles, 1, BK, 1) of block (n0 + rank NH) / FC_TB
+                        const int nc = n0 + (int)rank * Cfg::NH;
+                        tma_load_4d(ubase + su * Cfg::UF_BYTES, &tmU, fullU_bar(su), nc % FC_TB, z, kb * BK,
+                                    nc / FC_TB);
+                    }
                     if (++su == SU) {
                         su = 0;
                         pu ^= 1;
@@ -743,6 +755,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
+// U blocked by FC_TB tiles: dims (t, z, k, nb) = (FC_TB, Z, K, NP / FC_TB), box (b0, 1, b2, 1)
+bool encode_u4d(CUtensorMap *map, const void *ptr, uint64_t Z, uint64_t K, uint64_t NP, uint32_t b0, uint32_t b2,
+                CUtensorMapSwizzle swz) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {FC_TB, Z, K, NP / FC_TB};
+    cuuint64_t strides[3] = {FC_TB * 4, Z * FC_TB * 4, K * Z * FC_TB * 4};
+    cuuint32_t box[4] = {b0, 1, b2, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool encode_3d(CUtensorMap *map, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
                uint64_t s2_bytes, uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz,
                CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
@@ -773,7 +800,7 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     const uint64_t vZ = g.cplx ? 2 * (uint64_t)g.E : Z;
     if (!encode_3d(&mA, Vhi, vK, vM, vZ, Kp * 4, vM * Kp * 4, BK, 128, aswz) ||
         !encode_3d(&mAlo, Vlo, vK, vM, vZ, Kp * 4, vM * Kp * 4, BK, 128, aswz) ||
-        !encode_3d(&mB, U, NP, K, Z, NP * 4, K * NP * 4, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+        !encode_u4d(&mB, U, Z, K, NP, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     auto kern = nk3_gemm_tcgen05<CG, BLOCK_N, STAGES, BK>;
@@ -822,7 +849,7 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
         !encode_3d(&mAlo, Vlo, vK, vM, vZ, Kp * 2, vM * Kp * 2, Cfg::BK, 128, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
-        !encode_3d(&mU, U, NP, K, Z, NP * 4, K * NP * 4, Cfg::NH, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_u4d(&mU, U, Z, K, NP, Cfg::NH, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
         !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, SA, SU>;

@@ -11,7 +11,7 @@
 //
 // Layouts: n = (b*n_h + i)*n_w + j indexes tiles
 // (P:962-965), e = k*h + l indexes transformed elements.
-//   U [Z][K][BN_pad]   (tile index n contiguous -> coalesced along tiles)
+//   U [BN_pad/128][K][Z][128]   (blocked by 128 tiles, fc_u_off; n contiguous within a block)
 //   V [Z][M][Kp]       (K-major: the A operand of the contraction; Kp = K rounded up to 4)
 //   X [Z][M][BN_pad]
 // Winograd: Z=E, M=C', K=C.  Regular: Z=E, M=2C', K=2C (real embedding
@@ -179,7 +179,6 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
     }
     __syncthreads();
     // column pass along the H axis and store; nn fastest for coalescing
-    const size_t Kdim = g.K, BNp = g.BN_pad;
     float umx = 0.f;
     for (int idx = threadIdx.x; idx < TN * E; idx += blockDim.x) {
         const int nn = idx % TN, e = idx / TN;
@@ -199,19 +198,19 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
                 if (ph >= t) ph -= t;
             }
             if (g.method == CONV_REGULAR_FFT) {
-                U[((size_t)e * Kdim + c) * BNp + n] = ar;
-                U[((size_t)e * Kdim + g.C + c) * BNp + n] = ai;
+                U[fc_u_off(g, n, c, e)] = ar;
+                U[fc_u_off(g, n, g.C + c, e)] = ai;
             } else {
-                U[((size_t)e * Kdim + c) * BNp + n] = ar + ai;
-                U[((size_t)(E + e) * Kdim + c) * BNp + n] = ar;
-                U[((size_t)(2 * E + e) * Kdim + c) * BNp + n] = ai;
+                U[fc_u_off(g, n, c, e)] = ar + ai;
+                U[fc_u_off(g, n, c, E + e)] = ar;
+                U[fc_u_off(g, n, c, 2 * E + e)] = ai;
             }
             umx = fmaxf(umx, fabsf(ar) + fabsf(ai));
         } else {
             float a = 0.f;
             const float *zc = s_z + (size_t)nn * t * t + l;
             for (int aa = 0; aa < t; ++aa) a = fmaf(s_BT[k * t + aa], zc[aa * t], a);
-            U[((size_t)e * Kdim + c) * BNp + n] = a;
+            U[fc_u_off(g, n, c, e)] = a;
             umx = fmaxf(umx, fabsf(a));
         }
     }

@@ -120,11 +120,13 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
 // RED: also reduce max|U| into *g.umax (F16X3 contraction scale); 128-thread CTAs
 // capped at 64 registers so the reduction costs no occupancy.
 template <int T, bool RED>
+// cfast: grid (C, n-blocks) -- consecutive CTAs write consecutive channels of one U block,
+// i.e. one sequential run of Z * 512 bytes each (U is blocked by FC_TB = blockDim tiles)
 __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_wino(Geometry g, const float *__restrict__ in,
-                                                                     float *__restrict__ U) {
+                                                                     float *__restrict__ U, int cfast) {
     constexpr wtab::Tables tb = wtab::make(2, T - 1);  // B^T as literals (depends on t only)
-    const long long n_ = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int c = blockIdx.y;
+    const long long n_ = (long long)(cfast ? blockIdx.y : blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = cfast ? blockIdx.x : blockIdx.y;
     if (!RED && n_ >= g.BN) return;
     const bool valid = n_ < g.BN;
     const long long n = valid ? n_ : g.BN - 1;  // idle lanes recompute the last tile, store nothing
@@ -155,8 +157,7 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             for (int q = 0; q < T; ++q) s = wtab::cfma(tb.BT[l][q], d[a][q], s);
             z[a][l] = s;
         }
-    const size_t estride = (size_t)g.K * g.BN_pad;
-    float *dp = U + (size_t)c * g.BN_pad + n;
+    float *dp = U + fc_u_off(g, n, c, 0);  // element e at dp[e * FC_TB]: compile-time offsets
     float umx = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k)
@@ -165,9 +166,8 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             float s = -0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) s = wtab::cfma(tb.BT[k][a], z[a][l], s);
-            if (valid) *dp = s;  // plain store: U of an L2-resident chunk is re-read by NK3 from L2
+            if (valid) dp[(k * T + l) * FC_TB] = s;
             if (RED) umx = fmaxf(umx, fabsf(s));
-            dp += estride;
         }
     if (RED) fc_block_umax(g.umax, umx);
 }
@@ -525,7 +525,6 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
         }
     }
     __syncthreads();
-    const size_t estride = (size_t)g.K * g.BN_pad;
     float umx = 0.f;
     for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
         const int nn = it % FTN, l = it / FTN;
@@ -540,24 +539,22 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
         if (n >= g.BN) continue;
 #pragma unroll
         for (int k = 0; k < T; ++k) umx = fmaxf(umx, fabsf(z[k].x) + fabsf(z[k].y));
-        if (g.method == CONV_REGULAR_FFT) {
-            float *d0 = U + (size_t)c * g.BN_pad + n;
-            float *d1 = U + (size_t)(g.C + c) * g.BN_pad + n;
+        if (g.method == CONV_REGULAR_FFT) {  // rows c (Re) and C + c (Im), element e at + e * FC_TB
+            float *d0 = U + fc_u_off(g, n, c, l);
+            float *d1 = U + fc_u_off(g, n, g.C + c, l);
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                const size_t e = (size_t)(k * H + l) * estride;
-                d0[e] = z[k].x;
-                d1[e] = z[k].y;
+                d0[k * H * FC_TB] = z[k].x;
+                d1[k * H * FC_TB] = z[k].y;
             }
-        } else {  // Gauss: (U_r + U_i, U_r, U_i) in planes 0, 1, 2
-            float *d0 = U + (size_t)c * g.BN_pad + n;
-            const size_t pl = (size_t)g.E * estride;
+        } else {  // Gauss: (U_r + U_i, U_r, U_i) in element planes 0, 1, 2 (z = plane * E + e)
+            float *d0 = U + fc_u_off(g, n, c, l);
+            const size_t pl = (size_t)g.E * FC_TB;
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                const size_t e = (size_t)(k * H + l) * estride;
-                d0[e] = z[k].x + z[k].y;
-                d0[pl + e] = z[k].x;
-                d0[2 * pl + e] = z[k].y;
+                d0[k * H * FC_TB] = z[k].x + z[k].y;
+                d0[pl + k * H * FC_TB] = z[k].x;
+                d0[2 * pl + k * H * FC_TB] = z[k].y;
             }
         }
     }
@@ -803,7 +800,7 @@ __global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *_
                     for (int qq = 0; qq < T; ++qq) acc = wtab::cfma(tb.BT[l][qq], d[a][qq], acc);
                     z[a][l] = acc;
                 }
-            float *dp = U + (size_t)(c0 + gi) * g.BN_pad + (size_t)b * g.N + tile;
+            float *dp = U + fc_u_off(g, (long long)b * g.N + tile, c0 + gi, 0);
 #pragma unroll
             for (int kk = 0; kk < T; ++kk)
 #pragma unroll
@@ -811,9 +808,8 @@ __global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *_
                     float acc = -0.f;
 #pragma unroll
                     for (int a = 0; a < T; ++a) acc = wtab::cfma(tb.BT[kk][a], z[a][l], acc);
-                    *dp = acc;
+                    dp[(kk * T + l) * FC_TB] = acc;
                     if (RED) umx = fmaxf(umx, fabsf(acc));
-                    dp += estride;
                 }
         }
         __syncthreads();  // every thread is done with the slot
@@ -980,12 +976,19 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
     if (forward) {
         {
             static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
+            static const int cf_env = getenv("FASTCONV_NK2_NFAST") ? 0 : 1;
             if (g.umax) {
                 const unsigned nblk = (unsigned)((g.BN + 127) / 128);
-                nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst);
+                if (cf_env && nblk <= 65535)
+                    nk2_wino<T, true><<<dim3(g.C, nblk), 128, 0, s>>>(g, src, dst, 1);
+                else
+                    nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst, 0);
             } else {
                 const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
-                nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst);
+                if (cf_env && bs == FC_TB && nblk <= 65535)
+                    nk2_wino<T, false><<<dim3(g.C, nblk), bs, 0, s>>>(g, src, dst, 1);
+                else
+                    nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst, 0);
             }
         }
     } else {
