@@ -478,11 +478,12 @@ struct FftCfg {
 };
 
 template <int T>
-__global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U) {
+__global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U,
+                                                                 int cfast) {
     constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
     extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
-    const int c = blockIdx.y;
-    const long long n0 = (long long)blockIdx.x * FTN;
+    const int c = cfast ? blockIdx.x : blockIdx.y;
+    const long long n0 = (long long)(cfast ? blockIdx.y : blockIdx.x) * FTN;
     for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
         const int nn = it % FTN, p = it / FTN;
         const int a0 = 2 * p, a1 = 2 * p + 1;
@@ -667,7 +668,11 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
     if (forward) {
         const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
         fc_smem_attr((const void *)nk2_fft<T>, (int)smem);
-        nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst);
+        static const int cf = getenv("FASTCONV_NK2F_NFAST") ? 0 : 1;  // channel-fastest grid (measured faster)
+        if (cf && nblk <= 65535)
+            nk2_fft<T><<<dim3(g.C, nblk), 256, smem, s>>>(g, src, dst, 1);
+        else
+            nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst, 0);
     } else {
         // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
         // whole images when they fit (IPC images), else strips of R tile rows
