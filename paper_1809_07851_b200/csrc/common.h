@@ -60,15 +60,17 @@ struct conv_plan_s {
     conv_plan_info info;
 };
 
-// U layout, blocked by FC_TB tiles: U[nb][k][z][t] with n = nb * FC_TB + t, so one
-// NK2 CTA's (channel, 128 tiles) output is a single contiguous run of Z * 512 bytes
-// and consecutive transformed elements z sit 512 bytes apart (store immediates); the
-// contraction reads (128 tiles x 32 k) boxes of one (z, nb) with a 4-D tensor map.
-// BN_pad is a multiple of FC_TB.
+// U layout, blocked by FC_TB tiles: U[nb][z][k][t] with n = nb * FC_TB + t.  With a
+// channel-fastest NK2 grid, consecutive CTAs (channels k, k+1 of one 128-tile block) write
+// neighbouring 512-byte rows of every element slab, i.e. one sequential region per block;
+// the contraction's (128 tiles x 32 k) box of one (z, block) is a single contiguous 16 KB
+// run (4-D tensor map).  BN_pad is a multiple of FC_TB.
 #define FC_TB 128
 inline __host__ __device__ size_t fc_u_off(const Geometry &g, long long n, int k, int z) {
-    return (((size_t)(n / FC_TB) * g.K + k) * g.Z + z) * FC_TB + (size_t)(n % FC_TB);
+    return (((size_t)(n / FC_TB) * g.Z + z) * g.K + k) * FC_TB + (size_t)(n % FC_TB);
 }
+// stride (floats) between consecutive transformed elements z of one (tile, k)
+inline __host__ __device__ size_t fc_u_zs(const Geometry &g) { return (size_t)g.K * FC_TB; }
 
 // elements of V (one of V_hi / V_lo; fp32, or fp16 in F16X3 mode)
 inline size_t fc_v_floats(const Geometry &g) {

@@ -33,9 +33,9 @@ __global__ void __launch_bounds__(256) nk3_gemm_ffma(const float *__restrict__ A
             const int kk = i / BNT, col = i % BNT;
             const int gk = k0 + kk;
             const long long gn = n0 + col;
-            // U blocked by FC_TB tiles: U[n / TB][k][z][n % TB]
+            // U blocked by FC_TB tiles: U[n / TB][z][k][n % TB]
             Bs[kk][col] = (gk < K && gn < NP)
-                              ? Bm[(((size_t)(gn / FC_TB) * K + gk) * Zn + z) * FC_TB + (size_t)(gn % FC_TB)]
+                              ? Bm[(((size_t)(gn / FC_TB) * Zn + z) * K + gk) * FC_TB + (size_t)(gn % FC_TB)]
                               : 0.f;
         }
         __syncthreads();

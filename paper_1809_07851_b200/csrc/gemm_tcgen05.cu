@@ -757,11 +757,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // U blocked by FC_TB tiles: dims (t, z, k, nb) = (FC_TB, Z, K, NP / FC_TB), box (b0, 1, b2, 1)
 bool encode_u4d(CUtensorMap *map, const void *ptr, uint64_t Z, uint64_t K, uint64_t NP, uint32_t b0, uint32_t b2,
-                CUtensorMapSwizzle swz) {
+                CUtensorMapSwizzle swz) {  // U[nb][z][k][t] (fc_u_off)
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[4] = {FC_TB, Z, K, NP / FC_TB};
-    cuuint64_t strides[3] = {FC_TB * 4, Z * FC_TB * 4, K * Z * FC_TB * 4};
+    cuuint64_t strides[3] = {K * FC_TB * 4, FC_TB * 4, K * Z * FC_TB * 4};  // z, k, nb
     cuuint32_t box[4] = {b0, 1, b2, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void *>(ptr), dims, strides, box, estr,

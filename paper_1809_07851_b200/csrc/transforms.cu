@@ -11,7 +11,7 @@
 //
 // Layouts: n = (b*n_h + i)*n_w + j indexes tiles
 // (P:962-965), e = k*h + l indexes transformed elements.
-//   U [BN_pad/128][K][Z][128]   (blocked by 128 tiles, fc_u_off; n contiguous within a block)
+//   U [BN_pad/128][Z][K][128]   (blocked by 128 tiles, fc_u_off; n contiguous within a block)
 //   V [Z][M][Kp]       (K-major: the A operand of the contraction; Kp = K rounded up to 4)
 //   X [Z][M][BN_pad]
 // Winograd: Z=E, M=C', K=C.  Regular: Z=E, M=2C', K=2C (real embedding

@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             for (int q = 0; q < T; ++q) s = wtab::cfma(tb.BT[l][q], d[a][q], s);
             z[a][l] = s;
         }
-    float *dp = U + fc_u_off(g, n, c, 0);  // element e at dp[e * FC_TB]: compile-time offsets
+    float *dp = U + fc_u_off(g, n, c, 0);  // element e at dp[e * zs]
+    const size_t zs = fc_u_zs(g);
     float umx = 0.f;
 #pragma unroll
     for (int k = 0; k < T; ++k)
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             float s = -0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) s = wtab::cfma(tb.BT[k][a], z[a][l], s);
-            if (valid) dp[(k * T + l) * FC_TB] = s;
+            if (valid) dp[(k * T + l) * zs] = s;
             if (RED) umx = fmaxf(umx, fabsf(s));
         }
     if (RED) fc_block_umax(g.umax, umx);
@@ -540,22 +541,23 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
         if (n >= g.BN) continue;
 #pragma unroll
         for (int k = 0; k < T; ++k) umx = fmaxf(umx, fabsf(z[k].x) + fabsf(z[k].y));
-        if (g.method == CONV_REGULAR_FFT) {  // rows c (Re) and C + c (Im), element e at + e * FC_TB
+        const size_t zs = fc_u_zs(g);
+        if (g.method == CONV_REGULAR_FFT) {  // rows c (Re) and C + c (Im), element e at + e * zs
             float *d0 = U + fc_u_off(g, n, c, l);
             float *d1 = U + fc_u_off(g, n, g.C + c, l);
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                d0[k * H * FC_TB] = z[k].x;
-                d1[k * H * FC_TB] = z[k].y;
+                d0[k * H * zs] = z[k].x;
+                d1[k * H * zs] = z[k].y;
             }
         } else {  // Gauss: (U_r + U_i, U_r, U_i) in element planes 0, 1, 2 (z = plane * E + e)
             float *d0 = U + fc_u_off(g, n, c, l);
-            const size_t pl = (size_t)g.E * FC_TB;
+            const size_t pl = (size_t)g.E * zs;
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                d0[k * H * FC_TB] = z[k].x + z[k].y;
-                d0[pl + k * H * FC_TB] = z[k].x;
-                d0[2 * pl + k * H * FC_TB] = z[k].y;
+                d0[k * H * zs] = z[k].x + z[k].y;
+                d0[pl + k * H * zs] = z[k].x;
+                d0[2 * pl + k * H * zs] = z[k].y;
             }
         }
     }
@@ -813,7 +815,7 @@ __global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *_
                     float acc = -0.f;
 #pragma unroll
                     for (int a = 0; a < T; ++a) acc = wtab::cfma(tb.BT[kk][a], z[a][l], acc);
-                    dp[(kk * T + l) * FC_TB] = acc;
+                    dp[(kk * T + l) * fc_u_zs(g)] = acc;
                     if (RED) umx = fmaxf(umx, fabsf(acc));
                 }
         }

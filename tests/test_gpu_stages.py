@@ -70,8 +70,8 @@ def test_stages(fc, method, m, gemm, shape):
         Vhi = _ws_view(ws, p.layout["V"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].cpu()
         assert torch.all((Vhi.view(torch.int32) & 0x1FFF) == 0)
         V = V + _ws_view(ws, p.layout["Vlo"], Z * M * Kp).reshape(Z, M, Kp)[:, :, :K].double().cpu().numpy()
-    # U is blocked by 128 tiles: [BN_pad / 128][K][Z][128] (fc_u_off) -> [Z][K][BN]
-    U = (_ws_view(ws, p.layout["U"], Z * K * BNp).reshape(BNp // 128, K, Z, 128).permute(2, 1, 0, 3)
+    # U is blocked by 128 tiles: [BN_pad / 128][Z][K][128] (fc_u_off) -> [Z][K][BN]
+    U = (_ws_view(ws, p.layout["U"], Z * K * BNp).reshape(BNp // 128, Z, K, 128).permute(1, 2, 0, 3)
          .reshape(Z, K, BNp)[:, :, :BN].double().cpu().numpy())
     if gemm == "f16x3":  # NK2's reduction: exactly max|U| (Winograd), a bound |re|+|im| (FFT)
         umax = ws[p.layout["umax"]:p.layout["umax"] + 4].view(torch.float32).item()
