@@ -22,3 +22,33 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "vgg3_2"
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_fastconv_arm_json_line():
+    """The GPU arm of bench.py (short run) prints one JSON line with the contract's keys and
+    the roofline / e2e / clocks / gpu_launches objects filled from live measurements."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    res = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3", "--sweep-steps", "1",
+                          "--e2e-steps", "1", "--cpu-baseline-s", "1"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "clocks", "e2e",
+                "gpu_launches", "stages", "sweep"):
+        assert key in d, key
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] <= 1.2 and r["achieved"] > 0 and r["peak"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
+    assert d["gpu_launches"] >= 4 * d["steps"]
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["workload"] == "vgg3_2" and d["config"]["gemm"].startswith("tcgen05")
