@@ -274,6 +274,8 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         G.n_h = (G.Ho + m - 1) / m;
         G.n_w = (G.Wo + m - 1) / m;
         G.N = G.n_h * G.n_w;
+        G.divN = fc_fastdiv(G.N);
+        G.divNw = fc_fastdiv(G.n_w);
         G.E = G.t * G.h;
         G.BN = (long long)B * G.N;
         G.BN_pad = (G.BN + FC_TB - 1) / FC_TB * FC_TB;

@@ -25,6 +25,34 @@ struct ConvConsts {
     float sinv[FC_MAX_T];  // sin(2 pi j / t)
 };
 
+// Division by a runtime constant d >= 1 for dividends n < 2^31 (Granlund-Montgomery, as in
+// CUTLASS's FastDivmod): q = umulhi(n, mul) >> shift with p = 31 + ceil(log2 d),
+// mul = ceil(2^p / d) < 2^32 -- two instructions instead of a ~20-instruction division.
+struct FastDiv {
+    unsigned int mul, shift;
+    int d;
+};
+inline FastDiv fc_fastdiv(int d) {
+    FastDiv f;
+    f.d = d;
+    if (d <= 1) {  // q = n (fc_div tests d == 1)
+        f.mul = 0;
+        f.shift = 0;
+        return f;
+    }
+    int l = 0;
+    while ((1ll << l) < d) ++l;
+    const int p = 31 + l;
+    f.mul = (unsigned int)(((1ull << p) + (unsigned long long)d - 1) / (unsigned long long)d);
+    f.shift = (unsigned int)(p - 32);
+    return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ int fc_div(int n, const FastDiv &f) {
+    return f.d == 1 ? n : (int)(__umulhi((unsigned)n, f.mul) >> f.shift);
+}
+#endif
+
 struct Geometry {
     int B, C, Cout, H, W, r, m, method;
     int Ho, Wo, t, n_h, n_w, N, h, E, planes;
@@ -42,6 +70,7 @@ struct Geometry {
     float vbound;            // host bound: max|V[.][c'][.]| <= vbound * max|W[c']|
     unsigned int *umax;      // NK2 -> NK3 (nullptr: NK2 does not reduce)
     float *vscale;           // [2][Cout]: NK1 writes, NK3 epilogue reads the inverse
+    FastDiv divN, divNw;     // n -> (image, tile) and tile -> (row, column) in the transforms
 };
 
 struct conv_plan_s {

@@ -130,8 +130,9 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
     if (!RED && n_ >= g.BN) return;
     const bool valid = n_ < g.BN;
     const long long n = valid ? n_ : g.BN - 1;  // idle lanes recompute the last tile, store nothing
-    const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
-    const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+    // BN < 2^31 (U indices): fast divisions by the plan's constants N and n_w
+    const int b = fc_div((int)n, g.divN), tile = (int)n - b * g.N;
+    const int ti = fc_div(tile, g.divNw), tj = tile - ti * g.n_w;
     const int y0 = ti * g.m, x0 = tj * g.m;
     const float *src = in + ((size_t)b * g.C + c) * g.H * g.W + (size_t)y0 * g.W + x0;
     float d[T][T];
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
                 for (int l = 0; l < T; ++l) x[l] = __ldcs(sp + (size_t)(k * T + l) * estride);
             },
             y);
-        const int ti = tl / g.n_w, tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
+        const int ti = fc_div(tl, g.divNw), tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
         float *q0 = so + ti * m * SWo + tj * m;
 #pragma unroll
         for (int a = 0; a < MM; ++a) {
@@ -496,8 +497,8 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
         const long long n = n0 + nn;
         cf z[T];
         if (n < g.BN) {
-            const int b = (int)(n / g.N), tile = (int)(n - (long long)b * g.N);
-            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
+            const int b = fc_div((int)n, g.divN), tile = (int)n - b * g.N;
+            const int ti = fc_div(tile, g.divNw), tj = tile - ti * g.n_w;
             const int y0 = ti * g.m, x0 = tj * g.m;
             const float *src = in + ((size_t)b * g.C + c) * g.H * g.W;
             const bool r0 = y0 + a0 < g.H, r1 = (a1 < T) && (y0 + a1 < g.H);
