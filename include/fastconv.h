@@ -91,7 +91,7 @@ typedef struct {
     int E;              /* transformed elements per tile: t*t or t*h */
     int planes;         /* real planes per element: 1 Winograd, 2 Regular (re/im), 3 Gauss */
     long long BN;       /* B * N: rows of U_e / X_e */
-    long long BN_pad;   /* BN rounded up to 32 (row pitch of U and X) */
+    long long BN_pad;   /* BN rounded up to 128 (row pitch of U and X) */
     int gemm_Z, gemm_M, gemm_K;  /* batched contraction: Z products of [M x K] x [K x BN] */
     size_t bytes_U, bytes_V, bytes_X;   /* workspace tensors (V includes the hi/lo split) */
     size_t workspace_bytes;
@@ -107,6 +107,10 @@ typedef struct {
     int nchunks;        /* ceil(B / chunk) */
     int gemm;           /* the contraction implementation the plan runs (conv_gemm_impl;
                            CONV_GEMM_AUTO resolved; conv_plan_query reports AUTO's default) */
+    int x_planes;       /* real planes of X per transformed element: 1 Winograd, 2 Regular-FFT,
+                           3 Gauss-FFT (T1, T2, T3), or 2 when the F16X3 contraction combines
+                           Gauss in its epilogue (Re = T1 - T3, Im = T1 + T2; C' % 32 == 0;
+                           X is then [E][2C'][BN_pad] like Regular-FFT's); 0 for CONV_DIRECT */
 } conv_plan_info;
 
 /* Host-only: validate arguments and fill `info` (no CUDA calls).  Errors:

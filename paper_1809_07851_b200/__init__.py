@@ -45,7 +45,7 @@ class PlanInfo(ctypes.Structure):
                 [(n, ctypes.c_size_t) for n in ("bytes_U", "bytes_V", "bytes_X", "workspace_bytes")] +
                 [("alg_bytes", ctypes.c_double * 4), ("alg_flops", ctypes.c_double * 4),
                  ("direct_flops", ctypes.c_double), ("chunk", ctypes.c_int), ("nchunks", ctypes.c_int),
-                 ("gemm", ctypes.c_int)])
+                 ("gemm", ctypes.c_int), ("x_planes", ctypes.c_int)])
 
     def as_dict(self) -> dict:
         d = {}

@@ -17,6 +17,8 @@
 #include <new>
 
 #include <mutex>
+#include <algorithm>
+#include <map>
 #include <set>
 
 #include "common.h"
@@ -170,6 +172,26 @@ cudaError_t fc_smem_attr(const void *func, int bytes) {
     return e;
 }
 
+int fc_max_clusters(const void *func, const cudaLaunchConfig_t *cfg) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({func, dev});
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, func, cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[{func, dev}] = n;
+    if (getenv("FASTCONV_DEBUG_CLUSTERS"))
+        fprintf(stderr, "fastconv: kernel %p cluster %d x %d threads, %zu B smem: %d co-resident clusters\n", func,
+                cfg->numAttrs ? (int)cfg->attrs[0].val.clusterDim.x : 1, (int)cfg->blockDim.x, cfg->dynamicSmemBytes, n);
+    return n;
+}
+
 int fc_num_sms() {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
@@ -193,6 +215,30 @@ Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
 // launches pay wave tails and partial contraction tiles; profiles/r01_notes.md).
 // FASTCONV_CHUNK=<images> forces a chunk size (0 = whole batch);
 // FASTCONV_L2_BUDGET_MB=<MB> enables the budget heuristic.
+// Gauss epilogue combine: it saves one of X's three planes in NK3's writes and
+// NK4's reads, but three accumulators fit TMEM only as 128-column tiles, and those run the
+// F16X3 contraction ~1.35x slower per FLOP than 256-column tiles (per-SM operand traffic:
+// V' is re-staged per 128 columns).  Decide by the paper's stage-sum model for
+// NK3 + NK4 with B200 constants measured on this kernel set (profiles/r01_summary.md);
+// FASTCONV_GC=0/1 forces the choice.  G: Z, K, E, BN filled, Gauss-FFT.
+static bool gauss_combine_pays(const Geometry &G) {
+    const char *env = getenv("FASTCONV_GC");
+    if (env) return atoi(env) != 0;
+    if (getenv("FASTCONV_NO_GC")) return false;
+    const double bw = 6.5e12, bw4 = 4.9e12;     // HBM: streaming / NK4's achieved
+    const double r256 = 1.3e15, r128 = 0.95e15;  // F16X3 issue rate (3 fp16 products / FLOP)
+    const double BN = (double)G.BN, E = G.E, C = G.C, Co = G.Cout;
+    const double pad256 = std::ceil(BN / 256.0) * 256.0, pad128 = std::ceil(BN / 128.0) * 128.0;
+    const double mma = 3.0 * 6.0 * E * C * Co;  // tensor FLOPs per padded column
+    const double u = 4.0 * 3.0 * E * BN * C, x3 = 4.0 * 3.0 * E * BN * Co, x2 = x3 * 2.0 / 3.0;
+    const double o = 4.0 * G.B * Co * (double)G.Ho * G.Wo;
+    // the 3-plane contraction also drops to 128-column tiles when 256 would pad B N by >= 25%
+    const double r3 = 4.0 * pad256 >= 5.0 * pad128 ? mma * pad128 / r128 : mma * pad256 / r256;
+    const double t3 = std::max(r3, (u + x3) / bw) + (x3 + o) / bw4;
+    const double tgc = std::max(mma * pad128 / r128, (u + x2) / bw) + (x2 + o) / bw4;
+    return tgc < t3;
+}
+
 static int pick_chunk(const Geometry &G, size_t bytes_V) {
     if (G.method == CONV_DIRECT) return G.B;
     const char *env = getenv("FASTCONV_CHUNK");
@@ -203,7 +249,7 @@ static int pick_chunk(const Geometry &G, size_t bytes_V) {
     const char *benv = getenv("FASTCONV_L2_BUDGET_MB");
     if (!benv) return G.B;
     const double budget = atof(benv) * 1e6;
-    const double per_img = 4.0 * ((double)G.Z * G.K + (double)G.Z * G.M) * G.N;
+    const double per_img = 4.0 * ((double)G.Z * G.K + (double)G.Xz * G.Xm) * G.N;
     const double avail = budget - (double)bytes_V;
     long long bmax = avail > per_img ? (long long)(avail / per_img) : 1;
     if (bmax >= G.B) return G.B;
@@ -289,6 +335,9 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
         const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
         G.Kp = (G.K + kq - 1) / kq * kq;
+        G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G);
+        G.Xz = G.gc ? G.E : G.Z;
+        G.Xm = G.gc ? 2 * Cout : G.M;
         G.cplx = 0;
         if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % (G.vf16 ? 32 : 16) == 0 &&
             !getenv("FASTCONV_NO_CPLX")) {
@@ -308,6 +357,7 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         I.chunk = B;
         I.nchunks = 1;
         I.gemm = gemm == CONV_GEMM_AUTO ? CONV_GEMM_TCGEN05_F16X3 : gemm;
+        I.x_planes = method == CONV_DIRECT ? 0 : (G.gc ? 2 : G.planes);
         if (method != CONV_DIRECT) {
             const int split = (gemm != CONV_GEMM_FFMA);
             const size_t vb = fc_v_bytes(G);  // V_hi, then V_lo at the next 256 B boundary
@@ -319,7 +369,7 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
             const Geometry Gc = fc_chunk_geometry(G, I.chunk);
             I.BN_pad = Gc.BN_pad;
             I.bytes_U = (size_t)G.Z * G.K * Gc.BN_pad * 4;
-            I.bytes_X = (size_t)G.Z * G.M * Gc.BN_pad * 4;
+            I.bytes_X = (size_t)G.Xz * G.Xm * Gc.BN_pad * 4;
             I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
             // Table layer-stuff, c=C, c'=C', alpha=1; wE = reals per tile
             const double wE = (double)G.planes * G.E * (method == CONV_WINOGRAD ? 1 : 1);
@@ -330,8 +380,10 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
             (void)wE;
             I.alg_bytes[0] = 4.0 * CCp * r * r + 4.0 * wEr * CCp;
             I.alg_bytes[1] = 4.0 * B * C * (double)H * W + 4.0 * wEr * BCN;
-            I.alg_bytes[2] = 4.0 * wEr * (BN * C + CCp + BN * Cout);
-            I.alg_bytes[3] = 4.0 * wEr * BCpN + 4.0 * B * Cout * (double)G.Ho * G.Wo;
+            // X carries x_planes real planes per element (Gauss combined in NK3's epilogue: 2)
+            const double wX = G.gc ? 2.0 * G.E : wEr;
+            I.alg_bytes[2] = 4.0 * wEr * (BN * C + CCp) + 4.0 * wX * BN * Cout;
+            I.alg_bytes[3] = 4.0 * wX * BCpN + 4.0 * B * Cout * (double)G.Ho * G.Wo;
             // element-wise FLOPs: 2t^2 BNCC' / 8 t h BNCC' / 6 t h BNCC'
             const double k = method == CONV_WINOGRAD ? 2.0 : (method == CONV_REGULAR_FFT ? 8.0 : 6.0);
             I.alg_flops[2] = k * G.E * BN * CCp;

@@ -71,6 +71,11 @@ struct Geometry {
     unsigned int *umax;      // NK2 -> NK3 (nullptr: NK2 does not reduce)
     float *vscale;           // [2][Cout]: NK1 writes, NK3 epilogue reads the inverse
     FastDiv divN, divNw;     // n -> (image, tile) and tile -> (row, column) in the transforms
+    // X = [Xz][Xm][BN_pad]: Xz = Z, Xm = M, except the Gauss epilogue combine (gc = 1:
+    // F16X3, C' % 32 == 0), where the contraction stores Re = T1 - T3 and Im = T1 + T2
+    // as rows [0, C') / [C', 2C') of Xz = E planes -- the Regular-FFT layout
+    // ("X at w = 2")
+    int gc, Xz, Xm;
 };
 
 struct conv_plan_s {
@@ -219,6 +224,10 @@ Geometry fc_chunk_geometry(const Geometry &g, int Bc);
 cudaError_t fc_smem_attr(const void *func, int bytes);
 // SM count of the current device (persistent grids)
 int fc_num_sms();
+// clusters of `cfg`'s shape (cluster dims, block, dynamic smem) that can be co-resident on
+// the current device -- a persistent clustered grid larger than this runs in two waves
+// (cached per (kernel, device); 0 if the query fails)
+int fc_max_clusters(const void *func, const cudaLaunchConfig_t *cfg);
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
                              Geometry *g, conv_plan_info *info, conv_gemm_impl gemm);
 conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G);

@@ -445,8 +445,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // s_u = 2^(15 - e) with max|U| < 2^e (NK2's reduction), so |s_u U| < 2^15 and
 // no fp16 overflows; the epilogue multiplies each accumulator row by
 // 1 / (s_u s_v[c']) (exact powers of two) before the TMA store of X.
-template <int CG, int BLOCK_N, int SA, int SU>
+template <int CG, int BLOCK_N, int SA, int SU, bool GC = false>
 struct TcCfgF16 {
+    // GC (Gauss epilogue combine): the three products T1, T2, T3 of one (e, c', n) tile
+    // go to three of four TMEM accumulator slots, the epilogue stores Re = T1 - T3 and
+    // Im = T1 + T2 (two staging boxes per chunk); otherwise a double-buffered accumulator
+    static constexpr int NACC = GC ? 4 : 2;
+    static constexpr int SUB = GC ? 3 : 1;         // accumulators (products) per output tile
     static constexpr int BK = 32;              // K per stage (one 64 B swizzle row of fp16)
     static constexpr int BM = 128 * CG;
     static constexpr int NH = BLOCK_N / CG;    // tile columns (n) held per CTA
@@ -454,9 +459,9 @@ struct TcCfgF16 {
     static constexpr int UF_BYTES = NH * BK * 4;   // fp32 U as TMA lands it: [BK][NH]
     static constexpr int B_BYTES = NH * BK * 2;    // one fp16 split plane: [NH][BK] swizzled
     static constexpr int A_STAGE = 2 * A_BYTES + 2 * B_BYTES;  // MMA operands: V'_hi, V'_lo, U'_hi, U'_lo
-    static constexpr int TMEM_COLS = 2 * BLOCK_N;
-    static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
-    static constexpr int NBARS = 3 * SA + 2 * SU + 4;
+    static constexpr int TMEM_COLS = NACC * BLOCK_N;
+    static constexpr int EPI_BYTES = 4 * (GC ? 4 : 2) * 32 * 32 * 4;
+    static constexpr int NBARS = 3 * SA + 2 * SU + 2 * NACC;
     static constexpr int SMEM_BYTES = SA * A_STAGE + SU * UF_BYTES + EPI_BYTES + 1024 + 8 * NBARS + 16;
 };
 
@@ -470,15 +475,15 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // release as soon as they have converted a stage -- so the U loads from HBM run
 // SU stages ahead of the tensor cores instead of waiting for MMA completion.
 // Warp 0 lane 0 streams U, warp 2 lane 0 streams V (independent run-ahead).
-template <int CG, int BLOCK_N, int SA, int SU>
+template <int CG, int BLOCK_N, int SA, int SU, bool GC>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     nk3_gemm_tcgen05_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                          const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, int M,
                          int K, long long NP, int Z, int cplx, int Mh, int kb_half, int Cout,
                          const unsigned int *__restrict__ umax_p, const float *__restrict__ inv_sv) {
-    using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU>;
+    using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU, GC>;
     using I = Tc<CG>;
-    constexpr int BK = Cfg::BK;
+    constexpr int BK = Cfg::BK, NACC = Cfg::NACC, SUB = Cfg::SUB;
     static_assert(Cfg::TMEM_COLS <= 512, "TMEM holds 512 columns");
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -493,7 +498,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto fullU_bar = [&](int s) { return bar0 + 8u * (3 * SA + s); };      // fp32 U landed (tx)
     auto emptyU_bar = [&](int s) { return bar0 + 8u * (3 * SA + SU + s); };  // converted (4 local warps)
     auto tfull_bar = [&](int a) { return bar0 + 8u * (3 * SA + 2 * SU + a); };
-    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * SA + 2 * SU + 2 + a); };
+    auto tempty_bar = [&](int a) { return bar0 + 8u * (3 * SA + 2 * SU + NACC + a); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + (bar0 - base) + 8 * Cfg::NBARS);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -501,7 +506,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int grp = blockIdx.x / CG, ngrp = gridDim.x / CG;
     const int n_m = (M + Cfg::BM - 1) / Cfg::BM;
     const int n_n = (int)((NP + BLOCK_N - 1) / BLOCK_N);
-    const int num_tiles = Z * n_m * n_n;
+    // GC: Z = 3E products; an output tile (unit) is the element e's three sub-tiles z = e + p E
+    const int Zu = GC ? Z / 3 : Z;
+    const int num_tiles = Zu * n_m * n_n;
     const int num_k = (K + BK - 1) / BK;
 
     if (threadIdx.x == 0) {
@@ -514,7 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(fullU_bar(s), 1);
             mbar_init(emptyU_bar(s), 4);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < NACC; ++a) {
             mbar_init(tfull_bar(a), 1);
             mbar_init(tempty_bar(a), 4 * CG);
         }
@@ -542,9 +549,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int su = 0;
             uint32_t pu = 0;
             for (int T = grp; T < num_tiles; T += ngrp) {
-                int z, m0, n0;
-                decode(T, z, m0, n0);
+                int z0, m0, n0;
+                decode(T, z0, m0, n0);
+                for (int p = 0; p < SUB; ++p)
                 for (int kb = 0; kb < num_k; ++kb) {
+                    const int z = z0 + p * Zu;
                     mbar_wait(emptyU_bar(su), pu ^ 1);
                     mbar_expect_tx(fullU_bar(su), Cfg::UF_BYTES);
                     {  // U blocked by FC_TB tiles: box (NH tiles, 1, BK, 1) of block (n0 + rank NH) / FC_TB
@@ -564,9 +573,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int sa = 0;
             uint32_t pa = 0;
             for (int T = grp; T < num_tiles; T += ngrp) {
-                int z, m0, n0;
-                decode(T, z, m0, n0);
+                int z0, m0, n0;
+                decode(T, z0, m0, n0);
+                for (int p = 0; p < SUB; ++p)
                 for (int kb = 0; kb < num_k; ++kb) {
+                    const int z = z0 + p * Zu;
                     mbar_wait(emptyA_bar(sa), pa ^ 1);
                     const uint32_t sA = base + sa * Cfg::A_STAGE;
                     mbar_expect_tx(fullA_bar(sa), 2 * Cfg::A_BYTES);
@@ -594,7 +605,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t pa = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int T = grp; T < num_tiles; T += ngrp) {
+            for (int T = grp; T < num_tiles; T += ngrp)
+            for (int p = 0; p < SUB; ++p) {
                 mbar_wait(tempty_bar(acc), acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BLOCK_N;
@@ -625,13 +637,93 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 I::commit(tfull_bar(acc));
-                if (++acc == 2) {
+                if (++acc == NACC) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (GC && warp >= 4 && warp < 8) {
+        // ---- Gauss epilogue combine: Re = T1 - T3 -> X rows c', Im = T1 + T2 -> rows C' + c'
+        // of plane e; unscaled as above; two 32 x 32 boxes per chunk
+        const int q = warp & 3;
+        const uint32_t stage0 = epi0 + q * (4 * 4096);
+        const float inv_su = 1.f / fc_pow2_scale(__uint_as_float(*umax_p), 15);
+        int acc = 0, buf = 0;
+        uint32_t acc_phase = 0;
+        for (int T = grp; T < num_tiles; T += ngrp) {
+            int e, m0, n0;
+            decode(T, e, m0, n0);
+            const int row0 = m0 + 128 * (int)rank + q * 32;
+            const int cp = row0 + lane;
+            const float rs = cp < Cout ? inv_su * __ldg(inv_sv + cp) : 0.f;
+            int a[3];
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {  // the three slots of this tile, in issue order
+                a[p] = acc;
+                mbar_wait(tfull_bar(acc), acc_phase);
+                if (++acc == NACC) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+            tc_fence_after();
+            const bool live = row0 < Cout;  // C' % 32 == 0: a box is all-valid or all-outside
+#pragma unroll 1
+            for (int c = 0; c < BLOCK_N / 32; ++c) {
+                uint32_t v1[32], v2[32], v3[32];
+                const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16) + c * 32;
+                TMEM_LD_32(tl + a[0] * BLOCK_N, v1);
+                TMEM_LD_32(tl + a[1] * BLOCK_N, v2);
+                TMEM_LD_32(tl + a[2] * BLOCK_N, v3);
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const uint32_t sre = stage0 + buf * 8192, sim = sre + 4096;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float re[4], im[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float t1 = __uint_as_float(v1[4 * j + i]);
+                        re[i] = (t1 - __uint_as_float(v3[4 * j + i])) * rs;
+                        im[i] = (t1 + __uint_as_float(v2[4 * j + i])) * rs;
+                    }
+                    const uint32_t o = lane * 128 + ((j ^ (lane & 7)) << 4);
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sre + o), "f"(re[0]), "f"(re[1]),
+                                 "f"(re[2]), "f"(re[3])
+                                 : "memory");
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sim + o), "f"(im[0]), "f"(im[1]),
+                                 "f"(im[2]), "f"(im[3])
+                                 : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    if (live) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                &tmX),
+                            "r"(sre), "r"(n0 + 32 * c), "r"(row0), "r"(e)
+                            : "memory");
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                &tmX),
+                            "r"(sim), "r"(n0 + 32 * c), "r"(Cout + row0), "r"(e)
+                            : "memory");
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                buf ^= 1;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+#pragma unroll
+                for (int p = 0; p < 3; ++p) I::arrive_leader(tempty_bar(a[p]));
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else if (!GC && warp >= 4 && warp < 8) {
         // ---- epilogue: unscale by 1 / (s_u s_v[c']) and TMA-store X (as the tf32 kernel)
         const int q = warp & 3;
         const uint32_t stage0 = epi0 + q * (2 * 4096);
@@ -691,7 +783,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float su_scale = fc_pow2_scale(__uint_as_float(*umax_p), 15);
         int sa = 0, su = 0;
         uint32_t pa = 0, pu = 0;
-        for (int T = grp; T < num_tiles; T += ngrp) {
+        for (int T = grp; T < num_tiles; T += ngrp)
+        for (int p = 0; p < SUB; ++p) {
             for (int kb = 0; kb < num_k; ++kb) {
                 mbar_wait(fullU_bar(su), pu);
                 mbar_wait(fullA_bar(sa), pa);  // V landed => the operand slot is free (producer waited)
@@ -825,6 +918,10 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = CG > 1 ? 1 : 0;
+    if (CG > 1) {  // persistent: no more clusters than fit at once (else a second wave)
+        const int mc = fc_max_clusters((const void *)kern, &cfg);
+        if (mc > 0 && groups > mc) cfg.gridDim = dim3((unsigned)(CG * mc));
+    }
     int M_ = g.M, K_ = g.K, Z_ = g.Z;
     long long NP_ = g.BN_pad;
     int cplx_ = g.cplx, Mh_ = g.Cout, kbh_ = (g.C + BK - 1) / BK;
@@ -835,10 +932,10 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
 }
 
 
-template <int CG, int BLOCK_N, int SA, int SU>
+template <int CG, int BLOCK_N, int SA, int SU, bool GC = false>
 cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, const float *U, float *X,
                        cudaStream_t s) {
-    using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU>;
+    using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU, GC>;
     static_assert(Cfg::SMEM_BYTES <= 232448, "shared memory per CTA");
     CUtensorMap mA, mAlo, mU, mX;
     const uint64_t Z = (uint64_t)g.Z, M = (uint64_t)g.M, K = (uint64_t)g.K, NP = (uint64_t)g.BN_pad;
@@ -850,9 +947,11 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
         !encode_3d(&mAlo, Vlo, vK, vM, vZ, Kp * 2, vM * Kp * 2, Cfg::BK, 128, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
         !encode_u4d(&mU, U, Z, K, NP, Cfg::NH, Cfg::BK, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !encode_3d(&mX, X, NP, M, Z, NP * 4, M * NP * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+        !encode_3d(&mX, X, NP, (uint64_t)g.Xm, (uint64_t)g.Xz, NP * 4, (uint64_t)g.Xm * NP * 4, 32, 32,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
-    auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, SA, SU>;
+    if (GC && (g.Z != 3 * g.E || g.Xm != 2 * g.Cout || g.Cout % 32 != 0)) return cudaErrorInvalidValue;
+    auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, SA, SU, GC>;
     {
         cudaError_t e = fc_smem_attr((const void *)kern, Cfg::SMEM_BYTES);
         if (e != cudaSuccess) return e;
@@ -860,7 +959,7 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
     const int g_num_sms = fc_num_sms();
     const long long n_m = (g.M + Cfg::BM - 1) / Cfg::BM;
     const long long n_n = (g.BN_pad + BLOCK_N - 1) / BLOCK_N;
-    const long long tiles = (long long)g.Z * n_m * n_n;
+    const long long tiles = (long long)(GC ? g.E : g.Z) * n_m * n_n;
     const long long groups = tiles < g_num_sms / CG ? tiles : g_num_sms / CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(CG * groups));
@@ -874,6 +973,10 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = CG > 1 ? 1 : 0;
+    if (CG > 1) {  // persistent: no more clusters than fit at once (else a second wave)
+        const int mc = fc_max_clusters((const void *)kern, &cfg);
+        if (mc > 0 && groups > mc) cfg.gridDim = dim3((unsigned)(CG * mc));
+    }
     int M_ = g.M, K_ = g.K, Z_ = g.Z, Cout_ = g.Cout;
     long long NP_ = g.BN_pad;
     int cplx_ = g.cplx, Mh_ = g.Cout, kbh_ = (g.C + Cfg::BK - 1) / Cfg::BK;
@@ -903,6 +1006,14 @@ cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const
     if (!Vlo || !g.umax || !g.vscale) return cudaErrorInvalidValue;
     static const int force_1cta = getenv("FASTCONV_TC_1SM") != nullptr;
     // rings (operand stages, fp32 U stages): 4/4 measured 163 us vs 3/6 170 us on VGG-3.2 F(4,3)
+    if (g.gc) {  // Gauss epilogue combine: 4 accumulator slots of 128 columns
+        if (g.M > 128 && !force_1cta) return launch_f16<2, 128, 5, 4, true>(g, Vhi, Vlo, U, X, s);
+        return launch_f16<1, 128, 3, 3, true>(g, Vhi, Vlo, U, X, s);
+    }
+    // N = 256 tiles unless that pads B N by >= 25% more than N = 128 tiles would (small
+    // batches of few-tile images: deep FFT m = 14 has B N = 64, 4x / 2x padded)
+    const long long n256 = (g.BN + 255) / 256 * 256, n128 = (g.BN + 127) / 128 * 128;
+    if (g.M > 128 && !force_1cta && 4 * n256 >= 5 * n128) return launch_f16<2, 128, 5, 4>(g, Vhi, Vlo, U, X, s);
     if (g.M > 128 && !force_1cta) return launch_f16<2, 256, 4, 4>(g, Vhi, Vlo, U, X, s);
     return launch_f16<1, 128, 4, 4>(g, Vhi, Vlo, U, X, s);
 }

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) nk4_output_transform(Geometry g, const Co
     }
     const int co = blockIdx.y;
     const long long n0 = (long long)blockIdx.x * TN;
-    const size_t BNp = g.BN_pad, Mdim = g.M;
+    const size_t BNp = g.BN_pad, Mdim = g.Xm;
     for (int idx = threadIdx.x; idx < TN * E; idx += blockDim.x) {
         const int nn = idx % TN, e = idx / TN;
         const long long n = n0 + nn;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) nk4_output_transform(Geometry g, const Co
         if (n < g.BN) {
             if (g.method == CONV_WINOGRAD) {
                 xr = X[((size_t)e * Mdim + co) * BNp + n];
-            } else if (g.method == CONV_REGULAR_FFT) {
+            } else if (g.method == CONV_REGULAR_FFT || g.gc) {  // Gauss combined by NK3: Regular layout
                 xr = X[((size_t)e * Mdim + co) * BNp + n];
                 xi = X[((size_t)e * Mdim + g.Cout + co) * BNp + n];
             } else {

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     const int nimg = min(IPC, g.B - b);
     const int ntiles = nimg * ntr * g.n_w;  // contiguous in n
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
-    const size_t estride = (size_t)g.M * g.BN_pad;
+    const size_t estride = (size_t)g.Xm * g.BN_pad;
     const float *src0 = X + (size_t)co * g.BN_pad + nbase;
     for (int tl = threadIdx.x; tl < ntiles; tl += blockDim.x) {
         // stream the tile by rows of X (one row pair live at a time: registers / occupancy)
@@ -593,14 +593,14 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
     extern __shared__ float2 zs[];                                     // [ntiles][S]
     float *so = reinterpret_cast<float *>(zs + (size_t)IPC * R * g.n_w * S);  // [nimg*ntr*m][SWo]
-    const size_t estride = (size_t)g.M * g.BN_pad;
+    const size_t estride = (size_t)g.Xm * g.BN_pad;
     const size_t hstride = (size_t)H * estride;  // k -> k+1 along the element index e = k*H + l
     const float inv_nt = 1.f / (float)ntiles, inv_nw = 1.f / (float)g.n_w;
     for (int it = threadIdx.x; it < H * ntiles; it += blockDim.x) {
         const int l = fc_sdiv(it, inv_nt), tl = it - l * ntiles;
         cf z[T];
         const float *s0 = X + (size_t)co * g.BN_pad + nbase + tl + (size_t)l * estride;
-        if (g.method == CONV_REGULAR_FFT) {
+        if (g.method == CONV_REGULAR_FFT || g.gc) {  // (Re, Im) rows c', C' + c' (Gauss: combined by NK3)
             const float *s1 = s0 + (size_t)g.Cout * g.BN_pad;
 #pragma unroll
             for (int k = 0; k < T; ++k) z[k] = cf{__ldcs(s0 + k * hstride), __ldcs(s1 + k * hstride)};
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *_
     const int GN = G * g.N;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(bars);
-    const size_t estride = (size_t)g.M * g.BN_pad;
+    const size_t estride = (size_t)g.Xm * g.BN_pad;
     auto issue = [&](int q, int slot) {  // warp 0: lane j copies elements e = j, j + 32, ...
         const int co = q / gpc, b0 = (q - co * gpc) * G;
         const int ng = min(G, g.B - b0);

@@ -70,7 +70,7 @@ def test_geometry(lib, x, r, m, t, N):
         else:
             assert info["h"] == (t + 1 + 1) // 2 and info["E"] == t * ((t + 2) // 2)  # t*ceil((t+1)/2)
             assert info["planes"] == (2 if method == "regular_fft" else 3)
-        assert info["BN"] == 2 * N and info["BN_pad"] % 32 == 0 and info["BN_pad"] >= info["BN"]
+        assert info["BN"] == 2 * N and info["BN_pad"] % 128 == 0 and info["BN_pad"] >= info["BN"]
 
 
 def test_half_spectrum_size_t3(lib):
@@ -99,6 +99,30 @@ def test_algorithmic_costs_vgg32(lib):
     assert f14["alg_flops"][2] == pytest.approx(8 * th * B * 16 * C * Co)
     assert g14["alg_flops"][2] == pytest.approx(6 * th * B * 16 * C * Co)
     assert g14["alg_bytes"][1] - 4 * B * C * x * x == pytest.approx(1.5 * (f14["alg_bytes"][1] - 4 * B * C * x * x))
+    # X planes: on VGG-3.2 the stage-sum model keeps Gauss's three planes (T1, T2, T3): the
+    # combine's 128-column contraction tiles would cost more than the X plane saves
+    assert (w4["x_planes"], f14["x_planes"], g14["x_planes"]) == (1, 2, 3)
+    assert g14["alg_bytes"][2] == pytest.approx(4 * 3 * th * (B * 16 * C + C * Co + B * 16 * Co))
+
+
+def test_gauss_epilogue_combine_choice(lib, monkeypatch):
+    """where the plan combines Gauss in the contraction's epilogue (X at w = 2)
+    NK4 moves what Regular-FFT's does and NK3 writes 2/3 of the three-plane X."""
+    B, C, Co, x, r, th = 64, 64, 64, 226, 3, 16 * 9  # VGG-1.2, m = 14: HBM-bound, combined
+    g = fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14)
+    f = fc.plan_query(B, C, Co, x, x, r, "regular_fft", 14)
+    BN = B * 16 * 16
+    assert g["x_planes"] == 2 and g["bytes_X"] == 2 * th * Co * g["BN_pad"] * 4
+    assert g["alg_bytes"][3] == pytest.approx(f["alg_bytes"][3])
+    assert g["alg_bytes"][2] == pytest.approx(4 * 3 * th * (BN * C + C * Co) + 4 * 2 * th * BN * Co)
+    monkeypatch.setenv("FASTCONV_GC", "0")
+    g3 = fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14)
+    assert g3["x_planes"] == 3 and g3["bytes_X"] == 3 * th * Co * g3["BN_pad"] * 4
+    monkeypatch.setenv("FASTCONV_GC", "1")
+    assert fc.plan_query(64, 256, 256, 58, 58, 3, "gauss_fft", 14)["x_planes"] == 2
+    # C' % 32 != 0: never combined
+    g_odd = fc.plan_query(2, 8, 40, 20, 20, 3, "gauss_fft", 6)
+    assert g_odd["x_planes"] == 3 and g_odd["bytes_X"] == 3 * g_odd["E"] * 40 * g_odd["BN_pad"] * 4
 
 
 def _frac(v):

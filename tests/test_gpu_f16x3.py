@@ -101,3 +101,28 @@ def test_f16x3_not_less_accurate_than_3xtf32():
             e[gemm] = np.abs(y - O).max() / np.abs(O).max()
         print(method, m, e)
         assert e["f16x3"] <= 1.25 * e["tcgen05"], (method, m, e)
+
+
+@pytest.mark.parametrize("shape", [(2, 24, 64, 20, 19, 3), (3, 16, 160, 18, 18, 3), (2, 32, 96, 17, 23, 5),
+                                   (1, 8, 32, 12, 12, 3)])
+@pytest.mark.parametrize("m", [2, 6, 9])
+def test_gauss_epilogue_combine_equals_three_planes(shape, m, monkeypatch):
+    """with C' % 32 == 0 the F16X3 contraction stores Re = T1 - T3 and
+    Im = T1 + T2 instead of T1, T2, T3.  Scaling by 1/(s_u s_v) is a power of
+    two, so combining before or after it rounds identically: the output equals the
+    three-plane path (FASTCONV_GC=0) bit for bit, and meets the oracle bar."""
+    cfg = synth.custom(*shape, seed=94, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    monkeypatch.setenv("FASTCONV_GC", "1")
+    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "gauss_fft", m, "f16x3")
+    assert p.info["x_planes"] == 2
+    y = p.forward(I.cuda(), W.cuda()).cpu()
+    monkeypatch.setenv("FASTCONV_GC", "0")
+    p3 = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, "gauss_fft", m, "f16x3")
+    assert p3.info["x_planes"] == 3 and p3.info["bytes_X"] * 2 == p.info["bytes_X"] * 3
+    y3 = p3.forward(I.cuda(), W.cuda()).cpu()
+    torch.cuda.synchronize()
+    assert torch.equal(y, y3)
+    O = oracle.conv_fp64(I, W)
+    err = np.abs(y.double().numpy() - O).max() / np.abs(O).max()
+    assert err <= 1e-5, err
