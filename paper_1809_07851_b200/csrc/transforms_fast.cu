@@ -120,23 +120,37 @@ cudaError_t launch_nk1_wino(const Geometry &g, const ConvConsts &hc, const float
 // RED: also reduce max|U| into *g.umax (F16X3 contraction scale); 128-thread CTAs
 // capped at 64 registers so the reduction costs no occupancy.
 template <int T, bool RED>
-// cfast: grid (C, n-blocks) -- consecutive CTAs write consecutive channels of one U block,
-// i.e. one sequential run of Z * 512 bytes each (U is blocked by FC_TB = blockDim tiles)
-__global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_wino(Geometry g, const float *__restrict__ in,
-                                                                     float *__restrict__ U, int cfast) {
+// flags bit 0 (cfast): grid (C, n-blocks) -- consecutive CTAs write consecutive channels of
+// one U block, i.e. one sequential run of Z * 512 bytes each (U is blocked by FC_TB =
+// blockDim tiles); bit 1 (v2): even W and m, 8-byte aligned input -- every tile row starts
+// 8-byte aligned, load it as float2 (half the L1 requests of the overlapping lane accesses)
+__global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : (RED ? 4 : 1))
+    nk2_wino(Geometry g, const float *__restrict__ in, float *__restrict__ U, int flags) {
+    const int cfast = flags & 1;
     constexpr wtab::Tables tb = wtab::make(2, T - 1);  // B^T as literals (depends on t only)
     const long long n_ = (long long)(cfast ? blockIdx.y : blockIdx.x) * blockDim.x + threadIdx.x;
     const int c = cfast ? blockIdx.x : blockIdx.y;
     if (!RED && n_ >= g.BN) return;
-    const bool valid = n_ < g.BN;
-    const long long n = valid ? n_ : g.BN - 1;  // idle lanes recompute the last tile, store nothing
+    // idle lanes (RED: they take part in the CTA reduction) recompute the last tile and store
+    // the same values to the same addresses as its own lane -- no per-store predicate
+    const long long n = n_ < g.BN ? n_ : g.BN - 1;
     // BN < 2^31 (U indices): fast divisions by the plan's constants N and n_w
     const int b = fc_div((int)n, g.divN), tile = (int)n - b * g.N;
     const int ti = fc_div(tile, g.divNw), tj = tile - ti * g.n_w;
     const int y0 = ti * g.m, x0 = tj * g.m;
     const float *src = in + ((size_t)b * g.C + c) * g.H * g.W + (size_t)y0 * g.W + x0;
     float d[T][T];
-    if (y0 + T <= g.H && x0 + T <= g.W) {
+    // (t = 4 keeps scalar loads: float2 measured slower on VGG-1.2 F(2,3), NK2 0.82 -> 0.95+ ms)
+    if (T % 2 == 0 && T >= 6 && (flags & 2) && y0 + T <= g.H && x0 + T <= g.W) {
+#pragma unroll
+        for (int a = 0; a < T; ++a)
+#pragma unroll
+            for (int q = 0; q < T; q += 2) {
+                const float2 v = __ldg(reinterpret_cast<const float2 *>(src + a * g.W + q));
+                d[a][q] = v.x;
+                d[a][q + 1 < T ? q + 1 : q] = v.y;
+            }
+    } else if (y0 + T <= g.H && x0 + T <= g.W) {
 #pragma unroll
         for (int a = 0; a < T; ++a)
 #pragma unroll
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             for (int q = 0; q < T; ++q) s = wtab::cfma(tb.BT[l][q], d[a][q], s);
             z[a][l] = s;
         }
-    float *dp = U + fc_u_off(g, n, c, 0);  // element e at dp[e * zs]
+    float *dp = U + fc_u_off(g, n, c, 0);  // element e at dp[e * zs], stepped e by e
     const size_t zs = fc_u_zs(g);
     float umx = 0.f;
 #pragma unroll
@@ -168,7 +182,8 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : 1) nk2_
             float s = -0.f;
 #pragma unroll
             for (int a = 0; a < T; ++a) s = wtab::cfma(tb.BT[k][a], z[a][l], s);
-            if (valid) dp[(k * T + l) * zs] = s;
+            *dp = s;
+            dp += zs;
             if (RED) umx = fmaxf(umx, fabsf(s));
         }
     if (RED) fc_block_umax(g.umax, umx);
@@ -314,16 +329,24 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     const int nimg = min(IPC, g.B - b);
     const int ntiles = nimg * ntr * g.n_w;  // contiguous in n
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
-    const size_t estride = (size_t)g.Xm * g.BN_pad;
+    size_t ebytes = (size_t)g.Xm * g.BN_pad * sizeof(float);
+    asm("" : "+l"(ebytes));
     const float *src0 = X + (size_t)co * g.BN_pad + nbase;
     for (int tl = threadIdx.x; tl < ntiles; tl += blockDim.x) {
         // stream the tile by rows of X (one row pair live at a time: registers / occupancy)
         float y[MM][MM];
-        const float *sp = src0 + tl;
+        // element e = k T + l at sp[e * estride]; wino_out_tile asks for the rows in
+        // increasing k, so step the pointer by an opaque byte stride (one 64-bit add per
+        // load instead of a re-derived 64-bit index product)
+        const char *sp = reinterpret_cast<const char *>(src0 + tl);
         wino_out_tile<T, MM>(
             [&](int k, float *x) {
+                (void)k;
 #pragma unroll
-                for (int l = 0; l < T; ++l) x[l] = __ldcs(sp + (size_t)(k * T + l) * estride);
+                for (int l = 0; l < T; ++l) {
+                    x[l] = __ldcs(reinterpret_cast<const float *>(sp));
+                    sp += ebytes;
+                }
             },
             y);
         const int ti = fc_div(tl, g.divNw), tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
@@ -991,18 +1014,20 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
         {
             static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
             static const int cf_env = getenv("FASTCONV_NK2_NFAST") ? 0 : 1;
+            static const int v2_env = getenv("FASTCONV_NK2_NOV2") ? 0 : 1;
+            const int v2 = (v2_env && ((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
             if (g.umax) {
                 const unsigned nblk = (unsigned)((g.BN + 127) / 128);
                 if (cf_env && nblk <= 65535)
-                    nk2_wino<T, true><<<dim3(g.C, nblk), 128, 0, s>>>(g, src, dst, 1);
+                    nk2_wino<T, true><<<dim3(g.C, nblk), 128, 0, s>>>(g, src, dst, 1 | v2);
                 else
-                    nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst, 0);
+                    nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst, v2);
             } else {
                 const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
                 if (cf_env && bs == FC_TB && nblk <= 65535)
-                    nk2_wino<T, false><<<dim3(g.C, nblk), bs, 0, s>>>(g, src, dst, 1);
+                    nk2_wino<T, false><<<dim3(g.C, nblk), bs, 0, s>>>(g, src, dst, 1 | v2);
                 else
-                    nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst, 0);
+                    nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst, v2);
             }
         }
     } else {
