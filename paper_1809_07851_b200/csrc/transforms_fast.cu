@@ -508,10 +508,13 @@ struct FftCfg {
 };
 
 template <int T>
+// flags: bit 0 channel-fastest grid, bit 1 tile rows 8-byte aligned (even W and m, aligned
+// input): float2 row loads, half the L1 requests of the lanes' scattered 4-byte loads
 __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U,
-                                                                 int cfast) {
+                                                                 int flags) {
     constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
     extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
+    const int cfast = flags & 1;
     const int c = cfast ? blockIdx.x : blockIdx.y;
     const long long n0 = (long long)(cfast ? blockIdx.y : blockIdx.x) * FTN;
     for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
@@ -527,7 +530,15 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
             const bool r0 = y0 + a0 < g.H, r1 = (a1 < T) && (y0 + a1 < g.H);
             const float *row0 = src + (size_t)(y0 + a0) * g.W + x0;
             const float *row1 = row0 + g.W;
-            if (x0 + T <= g.W) {
+            if (T % 2 == 0 && (flags & 2) && x0 + T <= g.W) {
+#pragma unroll
+                for (int q = 0; q < T; q += 2) {
+                    const float2 u0 = r0 ? __ldg(reinterpret_cast<const float2 *>(row0 + q)) : make_float2(0.f, 0.f);
+                    const float2 u1 = r1 ? __ldg(reinterpret_cast<const float2 *>(row1 + q)) : make_float2(0.f, 0.f);
+                    z[q] = cf{u0.x, u1.x};
+                    z[q + 1 < T ? q + 1 : q] = cf{u0.y, u1.y};
+                }
+            } else if (x0 + T <= g.W) {
 #pragma unroll
                 for (int q = 0; q < T; ++q) {
                     z[q].x = r0 ? __ldg(row0 + q) : 0.f;
@@ -570,23 +581,28 @@ __global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, co
         if (n >= g.BN) continue;
 #pragma unroll
         for (int k = 0; k < T; ++k) umx = fmaxf(umx, fabsf(z[k].x) + fabsf(z[k].y));
-        const size_t zs = fc_u_zs(g);
-        if (g.method == CONV_REGULAR_FFT) {  // rows c (Re) and C + c (Im), element e at + e * zs
-            float *d0 = U + fc_u_off(g, n, c, l);
-            float *d1 = U + fc_u_off(g, n, g.C + c, l);
+        // element e = k H + l at + e * zs: step the pointers by an opaque byte stride
+        size_t hb = (size_t)H * fc_u_zs(g) * sizeof(float);
+        asm("" : "+l"(hb));
+        if (g.method == CONV_REGULAR_FFT) {  // rows c (Re) and C + c (Im)
+            char *d0 = reinterpret_cast<char *>(U + fc_u_off(g, n, c, l));
+            char *d1 = reinterpret_cast<char *>(U + fc_u_off(g, n, g.C + c, l));
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                d0[k * H * zs] = z[k].x;
-                d1[k * H * zs] = z[k].y;
+                *reinterpret_cast<float *>(d0) = z[k].x;
+                *reinterpret_cast<float *>(d1) = z[k].y;
+                d0 += hb;
+                d1 += hb;
             }
         } else {  // Gauss: (U_r + U_i, U_r, U_i) in element planes 0, 1, 2 (z = plane * E + e)
-            float *d0 = U + fc_u_off(g, n, c, l);
-            const size_t pl = (size_t)g.E * zs;
+            char *d0 = reinterpret_cast<char *>(U + fc_u_off(g, n, c, l));
+            const size_t pl = (size_t)g.E * fc_u_zs(g) * sizeof(float);
 #pragma unroll
             for (int k = 0; k < T; ++k) {
-                d0[k * H * zs] = z[k].x + z[k].y;
-                d0[pl + k * H * zs] = z[k].x;
-                d0[2 * pl + k * H * zs] = z[k].y;
+                *reinterpret_cast<float *>(d0) = z[k].x + z[k].y;
+                *reinterpret_cast<float *>(d0 + pl) = z[k].x;
+                *reinterpret_cast<float *>(d0 + 2 * pl) = z[k].y;
+                d0 += hb;
             }
         }
     }
@@ -617,6 +633,8 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     extern __shared__ float2 zs[];                                     // [ntiles][S]
     float *so = reinterpret_cast<float *>(zs + (size_t)IPC * R * g.n_w * S);  // [nimg*ntr*m][SWo]
     const size_t estride = (size_t)g.Xm * g.BN_pad;
+    // (stepping these loads by an opaque byte stride, as nk4_wino does, measured slower here:
+    // VGG-1.2 t = 27 / 32 NK4 +7-9%, three-plane Gauss +13%)
     const size_t hstride = (size_t)H * estride;  // k -> k+1 along the element index e = k*H + l
     const float inv_nt = 1.f / (float)ntiles, inv_nw = 1.f / (float)g.n_w;
     for (int it = threadIdx.x; it < H * ntiles; it += blockDim.x) {
@@ -701,10 +719,12 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
         fc_smem_attr((const void *)nk2_fft<T>, (int)smem);
         static const int cf = getenv("FASTCONV_NK2F_NFAST") ? 0 : 1;  // channel-fastest grid (measured faster)
+        static const int v2_env = getenv("FASTCONV_NK2_NOV2") ? 0 : 1;
+        const int v2 = (v2_env && ((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
         if (cf && nblk <= 65535)
-            nk2_fft<T><<<dim3(g.C, nblk), 256, smem, s>>>(g, src, dst, 1);
+            nk2_fft<T><<<dim3(g.C, nblk), 256, smem, s>>>(g, src, dst, 1 | v2);
         else
-            nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst, 0);
+            nk2_fft<T><<<dim3(nblk, g.C), 256, smem, s>>>(g, src, dst, v2);
     } else {
         // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
         // whole images when they fit (IPC images), else strips of R tile rows
