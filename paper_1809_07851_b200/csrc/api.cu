@@ -224,7 +224,6 @@ Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
 static bool gauss_combine_pays(const Geometry &G) {
     const char *env = getenv("FASTCONV_GC");
     if (env) return atoi(env) != 0;
-    if (getenv("FASTCONV_NO_GC")) return false;
     const double bw = 6.5e12, bw4 = 4.9e12;     // HBM: streaming / NK4's achieved
     const double r256 = 1.3e15, r128 = 0.95e15;  // F16X3 issue rate (3 fp16 products / FLOP)
     const double BN = (double)G.BN, E = G.E, C = G.C, Co = G.Cout;
