@@ -9,7 +9,7 @@ import json, re, sys
 v, pat = sys.argv[1], sys.argv[2]
 d = json.load(open('profiles/abv_configs.json'))
 print(v.ljust(6), ' '.join('%s/%s:%.4f[%s]' % (c[:5], k.replace('winograd', 'W').replace('regular_fft', 'R').replace('gauss_fft', 'G'),
-      r['ms'], ','.join('%.3f' % x for x in r['stage_ms'][1:])) for c, vv in d['configs'].items() for k, r in vv['runs'].items()
+      r['ms'], ','.join('%.3f' % x for x in r['stage_ms'])) for c, vv in d['configs'].items() for k, r in vv['runs'].items()
       if re.search(pat, k)))
 PY
 done; done

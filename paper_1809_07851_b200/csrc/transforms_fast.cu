@@ -428,15 +428,22 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
         }
     }
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
-    auto put = [&](int z, int row, int col, const float *v) {
-        const size_t o = (size_t)z * zstride + (size_t)row * g.Kp + col;
+    auto put = [&](size_t o, const float *v) {
         if (NC == 2)
             fc_store_v2(V, Vlo, o, v[0], v[NC - 1], sv);
         else
             fc_store_v(V, Vlo, o, v[0], split, sv);
     };
+    // offsets: ez = e * zstride for e = kk * H + l, stepped by an opaque H * zstride (one
+    // 64-bit add per kk instead of 64-bit index products per store)
+    size_t hz = (size_t)H * zstride;
+    asm("" : "+l"(hz));
+    size_t ez = (size_t)l * zstride;
+    const size_t o00 = (size_t)co * g.Kp + c;                          // (c', c)
+    const size_t o01 = o00 + g.C, o10 = o00 + (size_t)g.Cout * g.Kp;  // (c', C + c), (C' + c', c)
+    const size_t o11 = o10 + g.C, gpl = (size_t)g.E * zstride;
 #pragma unroll
-    for (int kk = 0; kk < T; ++kk) {
+    for (int kk = 0; kk < T; ++kk, ez += hz) {
         float vr[NC], vi[NC], t0[NC], t1[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
@@ -450,26 +457,25 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
             vr[j] = acc.x * inv;  // conj(DFT) / t^2
             vi[j] = -acc.y * inv;
         }
-        const int e = kk * H + l;
-        if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
-            put(2 * e, co, c, vr);
-            put(2 * e + 1, co, c, vi);
+        if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes z = 2e, 2e + 1
+            put(2 * ez + o00, vr);
+            put(2 * ez + zstride + o00, vi);
         } else if (g.method == CONV_REGULAR_FFT) {  // real embedding [[V_r, -V_i], [V_i, V_r]]
 #pragma unroll
             for (int j = 0; j < NC; ++j) t0[j] = -vi[j];
-            put(e, co, c, vr);
-            put(e, co, g.C + c, t0);
-            put(e, g.Cout + co, c, vi);
-            put(e, g.Cout + co, g.C + c, vr);
-        } else {  // Gauss: V_r, V_i - V_r, V_r + V_i
+            put(ez + o00, vr);
+            put(ez + o01, t0);
+            put(ez + o10, vi);
+            put(ez + o11, vr);
+        } else {  // Gauss: V_r, V_i - V_r, V_r + V_i in planes z = e, E + e, 2E + e
 #pragma unroll
             for (int j = 0; j < NC; ++j) {
                 t0[j] = vi[j] - vr[j];
                 t1[j] = vr[j] + vi[j];
             }
-            put(e, co, c, vr);
-            put(g.E + e, co, c, t0);
-            put(2 * g.E + e, co, c, t1);
+            put(ez + o00, vr);
+            put(ez + gpl + o00, t0);
+            put(ez + 2 * gpl + o00, t1);
         }
     }
 }
