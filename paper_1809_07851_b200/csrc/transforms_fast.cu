@@ -740,7 +740,9 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
             return (size_t)ipc * r * g.n_w * Sm * sizeof(float2) + (size_t)ipc * r * g.m * SWo * sizeof(float);
         };
         static const int items_env = getenv("FASTCONV_NK4F_ITEMS") ? atoi(getenv("FASTCONV_NK4F_ITEMS")) : 256;
-        const int target = items_env / H > 1 ? items_env / H : 1;
+        // at least 32 tiles per CTA: each (l, c') run of X a warp loads is then >= 128 bytes
+        // (VGG-1.2 m = 14 had 16-tile strips: 64-byte runs)
+        const int target = items_env / H > 32 ? items_env / H : 32;
         int R = target / g.n_w > 0 ? target / g.n_w : 1, IPC = 1;
         if (R >= g.n_h) {
             R = g.n_h;
