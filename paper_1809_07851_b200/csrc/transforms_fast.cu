@@ -311,7 +311,7 @@ __device__ __forceinline__ void wino_out_tile(LoadRow load_row, float (&y)[MM][M
 }
 
 // ----------------------------------------------------------- Winograd NK4 ---
-// CTA = (strip of R tile rows, output channel c', image b).  One thread per tile
+// CTA = (strip of R tile rows, image group, output channel c').  One thread per tile
 // loads its t^2 elements of X along n, computes Y = A^T X A, and writes the m x m
 // block into a shared-memory output strip; the CTA then stores the strip's
 // contiguous output rows with coalesced writes (crop to Ho x Wo on the way).
@@ -322,8 +322,7 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     extern __shared__ float so[];  // [img][ntr*m][SWo]
     const int m = g.m;
     // blockIdx.x = (image group, strip); IPC > 1 only with whole-image strips (R = n_h)
-    const int nstrip = (g.n_h + R - 1) / R;
-    const int strip = blockIdx.x % nstrip, b = (blockIdx.x / nstrip) * IPC, co = blockIdx.y;
+    const int strip = blockIdx.x, b = blockIdx.y * IPC, co = blockIdx.z;  // grid (strips, image groups, C')
     const int i0 = strip * R;
     const int ntr = min(R, g.n_h - i0);
     const int nimg = min(IPC, g.B - b);
@@ -629,8 +628,7 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     constexpr int H = FftCfg<T>::H;
     const int m = g.m;
     const int S = (m * H) % 2 ? m * H : m * H + 1;
-    const int nstrip = (g.n_h + R - 1) / R;
-    const int strip = blockIdx.x % nstrip, b = (blockIdx.x / nstrip) * IPC, co = blockIdx.y;
+    const int strip = blockIdx.x, b = blockIdx.y * IPC, co = blockIdx.z;  // grid (strips, image groups, C')
     const int i0 = strip * R;
     const int ntr = min(R, g.n_h - i0);
     const int nimg = min(IPC, g.B - b);
@@ -758,7 +756,8 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         const int ngroup = (g.B + IPC - 1) / IPC;
         const int items = H * IPC * R * g.n_w;
         const int threads = items >= 512 ? 512 : (items + 31) / 32 * 32;
-        nk4_fft<T><<<dim3(nstrip * ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
+        if (ngroup > 65535 || g.Cout > 65535) return cudaErrorInvalidConfiguration;
+        nk4_fft<T><<<dim3(nstrip, ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
     }
     return cudaGetLastError();
 }
@@ -1077,7 +1076,8 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
         fc_smem_attr((const void *)nk4_wino<T, MM>, 200 * 1024);
         const int tiles = IPC * R * g.n_w;
         const int threads = tiles >= 256 ? 256 : (tiles + 31) / 32 * 32;
-        nk4_wino<T, MM><<<dim3(nstrip * ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
+        if (ngroup > 65535 || g.Cout > 65535) return cudaErrorInvalidConfiguration;
+        nk4_wino<T, MM><<<dim3(nstrip, ngroup, g.Cout), threads, smem, s>>>(g, R, IPC, SWo, src, dst);
     }
     return cudaGetLastError();
 }
