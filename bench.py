@@ -117,6 +117,58 @@ class ClockSampler:
                 "power_w_max": max((num(p[3]) or 0.0) for p in used)}
 
 
+class NvmlProbe:
+    """Direct NVML reads (milliseconds each) taken while the queued timed steps execute, so
+    even a timed region shorter than nvidia-smi's 100 ms period carries clock samples."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.h = None
+
+    def sample(self):
+        if self.h is None:
+            return
+        try:
+            nv = self.nv
+            sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            try:
+                mask = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                mask = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+            pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+            self.samples.append((sm, mask, pw))
+        except Exception:
+            pass
+
+    def merge(self, clk: dict) -> dict:
+        """Fold the NVML samples into ClockSampler.summary()'s dict."""
+        if not self.samples:
+            return clk
+        sm = [x[0] for x in self.samples]
+        reasons = set(clk.get("reasons") or [])
+        reasons |= {n for (n, bit) in self.REASONS for (_, mask, _) in self.samples if mask & bit}
+        out = dict(clk)
+        smi = clk.get("samples_in_timed_region", 0) or 0
+        if not smi:  # no nvidia-smi sample fell inside the region: the NVML reads are the evidence
+            out["sm_mhz"] = statistics.median(sm)
+        out["sm_max_mhz"] = clk.get("sm_max_mhz") or self.max_sm
+        out["reasons"] = sorted(reasons)
+        out["nvml_samples_in_timed_region"] = len(sm)
+        out["nvml_sm_mhz_median"] = statistics.median(sm)
+        out["power_w_max"] = max(clk.get("power_w_max") or 0.0, max(x[2] for x in self.samples))
+        return out
+
+
 # --------------------------------------------------------------- reference ---
 def run_reference(args, rank, world):
     """The oracle as the reference arm: bounded samples of the workload on host cores."""
@@ -247,6 +299,9 @@ def main():
     out = torch.empty((cfg.B, cfg.Cout, cfg.Ho, cfg.Wo), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    clocks = ClockSampler(local)  # started before the sweep so it is streaming by the timed region
+    nvml = NvmlProbe(local)
+
     def time_plan(plan, ws, steps):
         for _ in range(2):
             plan.forward(x, w, out, ws)
@@ -290,7 +345,6 @@ def main():
     nst = 4 if method != "direct" else 1
 
     # ---- timed region -------------------------------------------------------------
-    clocks = ClockSampler(local)
     for _ in range(args.warmup):
         plan.forward(x, w, out, ws)
     torch.cuda.synchronize()
@@ -304,13 +358,16 @@ def main():
     start.record(stream)
     for k in range(args.steps):
         timer.forward(plan, x, w, out, ws)
+        if args.steps >= 200 and k == args.steps // 2:
+            nvml.sample()  # host-side read; hundreds of launches stay queued meanwhile
     end.record(stream)
+    nvml.sample()  # the queued steps are still running: a read inside the timed region
     torch.cuda.synchronize()
     parallel.barrier()
     t_wall1 = time.time()
     total_ms = start.elapsed_time(end)
     total_ms = parallel.max_over_ranks(total_ms, dev)
-    clk = clocks.summary(t_wall0, t_wall1)
+    clk = nvml.merge(clocks.summary(t_wall0, t_wall1))
     clocks.stop()
     ms_step = total_ms / args.steps
     stage_sum, nl = timer.read()
