@@ -355,8 +355,11 @@ def main():
     parallel.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]  # per-step spread
     start.record(stream)
     for k in range(args.steps):
+        if k:
+            step_ev[k].record(stream)
         timer.forward(plan, x, w, out, ws)
         if args.steps >= 200 and k == args.steps // 2:
             nvml.sample()  # host-side read; hundreds of launches stay queued meanwhile
@@ -366,6 +369,9 @@ def main():
     parallel.barrier()
     t_wall1 = time.time()
     total_ms = start.elapsed_time(end)
+    marks = [start] + step_ev[1:] + [end]
+    per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps))
+    step_stats = {"median": statistics.median(per_step), "min": per_step[0], "max": per_step[-1]}
     total_ms = parallel.max_over_ranks(total_ms, dev)
     clk = nvml.merge(clocks.summary(t_wall0, t_wall1))
     clocks.stop()
@@ -495,6 +501,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step_stats": {"rank0_median": step_stats["median"], "rank0_min": step_stats["min"],
+                                  "rank0_max": step_stats["max"],
+                                  "how": "CUDA events between consecutive steps of the timed region"},
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "B_per_gpu": cfg.B, "global_batch": cfg.B * world, "C": cfg.C,
                        "l2_chunk_images": info.get("chunk"), "l2_chunks": info.get("nchunks"),
