@@ -601,6 +601,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader CTA)
             // kind::f16: D f32 (bit 4), A = B = f16 (0), both K-major, N >> 3 at 17, M >> 4 at 24
             const uint32_t idesc0 = (1u << 4) | ((uint32_t)(BLOCK_N >> 3) << 17) | ((uint32_t)(Cfg::BM >> 4) << 24);
+            const uint64_t desc0 = make_desc(base, 16, 512, 4);
             int sa = 0;
             uint32_t pa = 0;
             int acc = 0;
@@ -615,16 +616,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     mbar_wait(split_bar(sa), pa);
                     tc_fence_after();
                     const uint32_t idesc = (re_tile && kb >= kb_half) ? (idesc0 | (1u << 13)) : idesc0;
-                    const uint32_t sA = base + sa * Cfg::A_STAGE;
-                    const uint32_t sAlo = sA + Cfg::A_BYTES;
-                    const uint32_t sB = sA + 2 * Cfg::A_BYTES;
-                    const uint32_t sBlo = sB + Cfg::B_BYTES;
+                    // descriptors = the stage-0 A_hi descriptor + (byte offset >> 4): the start
+                    // address is the descriptor's low field, so one add each (the single issuing
+                    // thread's per-MMA work bounds narrow tiles)
+                    const uint64_t dst = desc0 + (uint64_t)((uint32_t)(sa * Cfg::A_STAGE) >> 4);
 #pragma unroll
                     for (int s = 0; s < BK / 16; ++s) {  // K = 16 per instruction: +32 B in the 64 B row
-                        const uint64_t a_hi = make_desc(sA + 32 * s, 16, 512, 4);
-                        const uint64_t a_lo = make_desc(sAlo + 32 * s, 16, 512, 4);
-                        const uint64_t b_hi = make_desc(sB + 32 * s, 16, 512, 4);
-                        const uint64_t b_lo = make_desc(sBlo + 32 * s, 16, 512, 4);
+                        const uint64_t a_hi = dst + 2 * s;
+                        const uint64_t a_lo = dst + (Cfg::A_BYTES >> 4) + 2 * s;
+                        const uint64_t b_hi = dst + ((2 * Cfg::A_BYTES) >> 4) + 2 * s;
+                        const uint64_t b_lo = dst + ((2 * Cfg::A_BYTES + Cfg::B_BYTES) >> 4) + 2 * s;
                         const uint32_t first = (kb == 0 && s == 0) ? 0u : 1u;
                         I::mma_f16(d_tmem, a_lo, b_hi, idesc, first);
                         I::mma_f16(d_tmem, a_hi, b_lo, idesc, 1u);
