@@ -19,7 +19,8 @@
  * stage as E batched matrix products X_e = U_e V_e (NK3), and
  * inverse transform + crop (NK4).  Every stage is a hand-written
  * sm_100a CUDA kernel; the contraction runs on tcgen05 tensor cores with a
- * 3xTF32 split (or an FFMA fallback).
+ * two-term operand split (F16X3 by default, or 3xTF32; an FFMA fallback is
+ * selectable), and Gauss-FFT may be recombined in its epilogue (x_planes).
  *
  * Conventions for every entry point:
  *   - All tensors are fp32, contiguous, row-major: in [B][C][H][W],
