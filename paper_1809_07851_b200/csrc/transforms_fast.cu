@@ -514,8 +514,11 @@ struct FftCfg {
 
 template <int T>
 // flags: bit 0 channel-fastest grid, bit 1 tile rows 8-byte aligned (even W and m, aligned
-// input): float2 row loads, half the L1 requests of the lanes' scattered 4-byte loads
-__global__ void __launch_bounds__(256, (T <= 18) ? 4 : 0) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U,
+// input): float2 row loads, half the L1 requests of the lanes' scattered 4-byte loads.
+// 48 registers (5 CTAs/SM) for the composite t <= 16 codelets -- the kernel waits on its
+// loads, more resident warps help (VGG-3.2 t = 10 NK2 172 -> 144 us, t = 16 119 -> 112 us);
+// the prime-length DFTs (t = 11, 13) keep 64 (t = 13 measured 51 -> 64 us at 48)
+__global__ void __launch_bounds__(256, ((T <= 16 && T % 2 == 0) || T == 9) ? 5 : ((T <= 18) ? 4 : 0)) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U,
                                                                  int flags) {
     constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
     extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
