@@ -3,22 +3,32 @@
 "ms/layer & effective TFLOP/s (direct-conv FLOPs) + roofline fraction, 1/2/4/8 B200").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fastconv|reference]
+                    [--workload vgg3_2|vgg1_2|k5|deep|tiny] [--scaling strong|weak]
+                    [--flush-l2 auto|on|off] [--method M --m m] [--gemm auto|f16x3|tcgen05|ffma]
 
 A *step* is one full pass of the hot path: NK1 kernel transform,
 NK2 input transform, NK3 contraction, NK4 output transform + crop, over one batch
 of the workload (the paper times the kernel transform as part of the layer,
 P:455-460; reading R13).  Workload: BASELINE.json configs[1], the
-VGG-3.2-shaped layer (B=64 per GPU, C=C'=256, 58x58, r=3).  The (method, m) is
-chosen per the paper's comparison rule (each method at its fastest m):
-every (method, m) the config lists is timed briefly, the fastest is the headline
-and all are reported under "sweep".
+VGG-3.2-shaped layer (B=64, C=C'=256, 58x58, r=3).  The (method, m) is chosen
+per the paper's comparison rule (each method at its fastest m): every
+(method, m) the config lists is timed briefly, the fastest is the headline and
+all are reported under "sweep".
+
+Multi-GPU: ``--gpus N`` without torchrun re-launches this script
+under ``torch.distributed.run`` with N ranks (one per GPU); under torchrun,
+WORLD_SIZE must equal N.  Strong scaling (default): ONE global seeded draw of the
+config's B images; rank k owns images parallel.shard_range(B, k, N) and runs
+conv_plan(B_k, ...), transforming the kernels locally -- no collective on the data
+path.  ``--scaling weak`` draws B*N images once and gives every rank B of them.
 
 Timing: inputs resident in HBM; W untimed warm-up steps; K steps bracketed by a
 barrier + cuda synchronize on both sides, timed with CUDA events on the launching
-stream, max over ranks.  Inputs (221 MB per GPU) exceed the 126 MB L2, so no
-explicit flush.  nvidia-smi samples SM clocks and throttle reasons during the run.
-N > 1: launched by torchrun, one rank per GPU, every rank processes its own
-B=64 batch (weak scaling, no collective on the data path).
+stream, max over ranks.  L2: when a rank's inputs + outputs are smaller than 2x
+the 126 MB L2 (``--flush-l2 auto``), a 2x-L2 buffer is written between timed
+steps and only the steps themselves are timed (per-step events); otherwise the
+inputs are larger than L2 and no flush is needed.  nvidia-smi and NVML sample SM
+clocks and throttle reasons during the run.
 
 ``--impl reference`` times the fp64 CPU oracle (oracle/, the only other place this
 script runs it) on bounded samples of the same workload: the paper has no GPU
@@ -45,15 +55,6 @@ UNIT = "TFLOP/s"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 TF32_OVER_BF16 = 0.5  # nominal dense ratio (1.1 vs 2.25 PFLOP/s, B200_PROFILING.md)
 F16_OVER_BF16 = 1.0   # kind::f16 (fp16 in, fp32 accumulate) runs at the bf16 dense rate
-
-
-def contraction_peak(gemm: str, bf16_burst: float):
-    """fp32-equivalent TFLOP/s ceiling of NK3: three tensor-core products per fp32 product."""
-    if gemm == "tcgen05_f16x3":
-        return bf16_burst * F16_OVER_BF16 / 3.0, "bf16 burst x 1.0 (FP16/BF16 nominal) / 3 (F16X3 split)"
-    if gemm == "ffma":
-        return None, "FFMA (no tensor peak)"
-    return bf16_burst * TF32_OVER_BF16 / 3.0, "bf16 burst x 0.5 (TF32/BF16 nominal) / 3 (3xTF32 split)"
 
 
 def load_peaks():
@@ -254,6 +255,104 @@ def cpu_direct_baseline(cfg, seconds: float):
 
 
 # ------------------------------------------------------------------- main ---
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """--gpus N without a torchrun environment: run this script as N ranks (one per GPU)."""
+    # "--m" is an ambiguous prefix of torchrun's own options: pass it on as "--tile"
+    argv = ["--tile" if a == "--m" else ("--tile=" + a[4:] if a.startswith("--m=") else a) for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % n,
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def measure_matmul_peaks(dev, sustained_s: float = 1.5) -> dict:
+    """Dense tensor-core peaks measured like MEASURED_PEAKS.json's bf16 figure:
+    torch.matmul at 8192^3, best of 10 (burst) and back to back for `sustained_s` (sustained),
+    for fp32 inputs with TF32 allowed (the 3xTF32 contraction's pipe) and for fp16 (F16X3's)."""
+    import torch
+    out = {}
+    n = 8192
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        for name, dt in (("tf32", torch.float32), ("fp16", torch.float16)):
+            a = torch.randn(n, n, device=dev, dtype=dt)
+            b = torch.randn(n, n, device=dev, dtype=dt)
+            for _ in range(3):
+                torch.matmul(a, b)
+            best = 1e30
+            for _ in range(10):
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record()
+                torch.matmul(a, b)
+                s1.record()
+                s1.synchronize()
+                best = min(best, s0.elapsed_time(s1))
+            burst = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+            reps = max(5, int(sustained_s * 1e3 / best))
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(reps):
+                torch.matmul(a, b)
+            s1.record()
+            s1.synchronize()
+            sus = 2.0 * n ** 3 * reps / (s0.elapsed_time(s1) * 1e-3) / 1e12
+            out[name] = {"burst_tflops": burst, "sustained_tflops": sus}
+            del a, b
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    torch.cuda.empty_cache()
+    out["how"] = ("torch.matmul 8192^3 (cuBLAS), 2 n^3 FLOPs: best of 10 (burst), back to back for %.1f s "
+                  "(sustained); tf32 = fp32 inputs with allow_tf32" % sustained_s)
+    return out
+
+
+class StepTimer:
+    """The timed region: K steps on `stream`, bracketed by barrier + synchronize.  Without a
+    flush one event pair spans the K back-to-back steps; with a flush (2x L2 written between
+    steps) each step has its own pair and ms/step is the mean of the steps alone."""
+
+    def __init__(self, dev, stream, flush: bool):
+        import torch
+        self.torch = torch
+        self.stream = stream
+        self.flush = flush
+        self.buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+
+    def run(self, steps: int, fn, on_step=None):
+        torch = self.torch
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(self.stream)
+        for k in range(steps):
+            if self.flush:
+                self.buf.fill_(float(k))
+            ev[k][0].record(self.stream)
+            fn()
+            ev[k][1].record(self.stream)
+            if on_step:
+                on_step(k)
+        end.record(self.stream)
+        end.synchronize()
+        per = [a.elapsed_time(b) for a, b in ev]
+        if self.flush:
+            total = sum(per)
+        else:  # back to back: the span from the first step's start to the last step's end
+            total = ev[0][0].elapsed_time(ev[-1][1])
+        return total, per
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -262,13 +361,16 @@ def main():
     ap.add_argument("--impl", default="fastconv", choices=["fastconv", "reference"])
     ap.add_argument("--workload", default="vgg3_2")
     ap.add_argument("--method", default="auto", help="auto (sweep) or winograd|regular_fft|gauss_fft|direct")
-    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--m", "--tile", dest="m", type=int, default=0)
     ap.add_argument("--gemm", default="auto", choices=["auto", "tcgen05", "ffma", "f16x3"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-baseline-s", type=float, default=12.0)
     ap.add_argument("--reference-budget-s", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the 3xTF32 arm, cached/graph runs, peaks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -279,40 +381,56 @@ def main():
             parallel.init("gloo")
         run_reference(args, rank, world)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    if world != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world), file=sys.stderr)
+        sys.exit(2)
 
     import torch
     import synth
     import paper_1809_07851_b200 as fc
-    rank, world, local = parallel.init()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        print("bench.py: no CUDA device", file=sys.stderr)
+        sys.exit(1)
+    # one rank per GPU; with fewer GPUs than ranks (a dry multi-rank run on one box) ranks share
+    # devices, the data path still has no collective, and the line says "oversubscribed"
+    oversub = world > ndev
+    dev_index = local % ndev
+    rank, world, local = parallel.init("gloo" if oversub else None)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     fc.load()
-    cfg = synth.CONFIGS[args.workload]
+    base = synth.CONFIGS[args.workload]
     peaks, peaks_src = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     bf16_burst = float(peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"]))
-    tf32_peak = bf16_burst * TF32_OVER_BF16
 
-    # weak scaling: every rank owns a full B-image batch (independent seeded draw per rank)
-    I, W = synth.make_inputs(cfg, seed=cfg.seed + 1000 * rank)
+    # one global seeded draw; rank k slices its images (strong: B/N each, weak: B each)
+    gcfg = base if args.scaling == "strong" else base.with_batch(base.B * world)
+    I_all, W = synth.make_inputs(gcfg)
+    lo, hi = parallel.shard_range(gcfg.B, rank, world)
+    I = I_all[lo:hi].contiguous()
+    del I_all
+    cfg = base.with_batch(hi - lo)  # this rank's layer
+    job_flops = gcfg.direct_flops  # whole-job direct-conv FLOPs per step
     x, w = I.to(dev), W.to(dev)
     out = torch.empty((cfg.B, cfg.Cout, cfg.Ho, cfg.Wo), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    io_bytes = (I.numel() + W.numel() + out.numel()) * 4
+    flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and io_bytes < 2 * L2_BYTES)
+    timer_fn = StepTimer(dev, stream, flush)
 
-    clocks = ClockSampler(local)  # started before the sweep so it is streaming by the timed region
-    nvml = NvmlProbe(local)
+    clocks = ClockSampler(dev_index)  # started before the sweep so it is streaming by the timed region
+    nvml = NvmlProbe(dev_index)
 
     def time_plan(plan, ws, steps):
         for _ in range(2):
             plan.forward(x, w, out, ws)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        s.record(stream)
-        for _ in range(steps):
-            plan.forward(x, w, out, ws)
-        e.record(stream)
-        e.synchronize()
-        return s.elapsed_time(e) / steps
+        total, _ = timer_fn.run(steps, lambda: plan.forward(x, w, out, ws))
+        return total / steps
 
     # ---- sweep (the paper's rule: each method at its fastest m) -----------------
     runs = list(cfg.runs) if args.method == "auto" else [(args.method, args.m)]
@@ -320,12 +438,12 @@ def main():
     for method, m in runs:
         plan = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, args.gemm)
         ws = plan.alloc_workspace(dev)
-        ms = parallel.max_over_ranks(time_plan(plan, ws, args.sweep_steps), dev)
+        ms = parallel.max_over_ranks(time_plan(plan, ws, args.sweep_steps), dev if not oversub else None)
         prof = [plan.forward_profiled(x, w, out, ws) for _ in range(3)]
         stage_ms_sweep = [round(min(p[s] for p in prof), 4) for s in range(4)]
-        sweep["%s/m=%d" % (method, m)] = {"method": method, "m": m, "t": plan.info["t"], "ms": ms,
-                                         "tflops": cfg.direct_flops * world / (ms * 1e-3) / 1e12,
-                                         "stage_ms": stage_ms_sweep}
+        sweep["%s/m=%d" % (method, plan.info["m"])] = {
+            "method": method, "m": plan.info["m"], "t": plan.info["t"], "ms": ms,
+            "tflops": job_flops / (ms * 1e-3) / 1e12, "stage_ms": stage_ms_sweep}
         del ws, plan
         torch.cuda.empty_cache()
     best = min(sweep.values(), key=lambda d: d["ms"])
@@ -336,12 +454,30 @@ def main():
     ws = plan.alloc_workspace(dev)
     info = plan.info
     gemm_name = fc.GEMM_NAMES.get(info["gemm"], args.gemm)
-    c_peak, c_peak_src = contraction_peak(gemm_name, bf16_burst)
+    # the tensor-pipe peaks are measured after the timed region (cuBLAS at full power heats the
+    # part and would push the timed steps into the power cap); until then: nominal ratios
+    PK = {"fp16": bf16_burst * F16_OVER_BF16, "tf32": bf16_burst * TF32_OVER_BF16, "measured": None}
+
+    def contraction_peak_of(gname):
+        mm = PK["measured"]
+        if gname == "tcgen05_f16x3":
+            return PK["fp16"] / 3.0, ("measured fp16 matmul burst / 3 (F16X3 split)" if mm else
+                                      "bf16 burst x 1.0 (FP16/BF16 nominal) / 3 (F16X3 split)")
+        if gname == "ffma":
+            return None, "FFMA (no tensor peak)"
+        return PK["tf32"] / 3.0, ("measured tf32 matmul burst / 3 (3xTF32 split)" if mm else
+                                  "bf16 burst x 0.5 (TF32/BF16 nominal) / 3 (3xTF32 split)")
+
+    c_peak, c_peak_src = contraction_peak_of(gemm_name)
     plan_report = planner.report(
-        {(d["method"], d["m"]): fc.plan_query(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, d["method"], d["m"])
+        {(d["method"], d["m"]): fc.plan_query(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, d["method"], d["m"],
+                                              args.gemm)
          for d in sweep.values() if d["method"] != "direct"},
         {(d["method"], d["m"]): d["ms"] for d in sweep.values()},
-        hbm_peak, c_peak or tf32_peak / 3.0)
+        hbm_peak, c_peak or PK["tf32"] / 3.0)
+    if method != "direct":
+        mb, mb_ms, _ = fc.best_m(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, args.gemm)
+        plan_report["conv_plan_best_m"] = {"method": method, "m": mb, "model_ms": mb_ms}
     nst = 4 if method != "direct" else 1
 
     # ---- timed region -------------------------------------------------------------
@@ -351,37 +487,136 @@ def main():
     # per-launch CUDA events recorded by the library itself (conv_forward_timed): the
     # timed loop runs exactly the launches of conv_forward, with no host sync inside
     timer = fc.StageTimer((plan.launches + 1) * args.steps + 8)  # + 1 start marker per call
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def on_step(k):
+        if args.steps >= 200 and k == args.steps // 2:
+            nvml.sample()  # host-side read; hundreds of launches stay queued meanwhile
+
     parallel.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
-    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]  # per-step spread
-    start.record(stream)
-    for k in range(args.steps):
-        if k:
-            step_ev[k].record(stream)
-        timer.forward(plan, x, w, out, ws)
-        if args.steps >= 200 and k == args.steps // 2:
-            nvml.sample()  # host-side read; hundreds of launches stay queued meanwhile
-    end.record(stream)
-    nvml.sample()  # the queued steps are still running: a read inside the timed region
+    total_ms, per_step = timer_fn.run(args.steps, lambda: timer.forward(plan, x, w, out, ws), on_step)
+    nvml.sample()
     torch.cuda.synchronize()
     parallel.barrier()
     t_wall1 = time.time()
-    total_ms = start.elapsed_time(end)
-    marks = [start] + step_ev[1:] + [end]
-    per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps))
+    per_step = sorted(per_step)
     step_stats = {"median": statistics.median(per_step), "min": per_step[0], "max": per_step[-1]}
-    total_ms = parallel.max_over_ranks(total_ms, dev)
+    rank_ms = total_ms / args.steps
+    ms_step = parallel.max_over_ranks(rank_ms, dev if not oversub else None)
+    rank_ms_all = parallel.all_gather_scalar(rank_ms, dev if not oversub else None)
     clk = nvml.merge(clocks.summary(t_wall0, t_wall1))
     clocks.stop()
-    ms_step = total_ms / args.steps
     stage_sum, nl = timer.read()
-    # per step: each stage's launches (NK2-4 run once per L2 chunk) summed
+    # per step: each stage's launches (NK2-4 run once per chunk) summed
     stage_ms = [stage_sum[s] / args.steps for s in range(4)] if nst == 4 else [stage_sum[2] / args.steps]
-    value = cfg.direct_flops * world / (ms_step * 1e-3) / 1e12
+    value = job_flops / (ms_step * 1e-3) / 1e12
 
+    extras = {}
+    if not args.no_extras and nst == 4:
+        extras = run_extras(args, fc, cfg, plan, x, w, out, ws, stream, timer_fn, job_flops, world, dev, oversub,
+                            hbm_peak, contraction_peak_of, method, m, parallel)
+
+    # ---- end to end through the public API (host buffers, copies in the region) ---
+    hi_, hw_ = I.pin_memory(), W.pin_memory()
+    ho_ = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
+    torch.cuda.synchronize()
+    parallel.barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.e2e_steps):
+        plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = parallel.max_over_ranks(s0.elapsed_time(s1) / args.e2e_steps, dev if not oversub else None)
+    h2d_job = parallel.sum_over_ranks(float(I.numel() * 4 + W.numel() * 4), dev if not oversub else None)
+    d2h_job = parallel.sum_over_ranks(float(out.numel() * 4), dev if not oversub else None)
+    e2e = {"value": job_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": int(h2d_job), "d2h_bytes_per_step": int(d2h_job),
+           "api": "conv_forward_host (pinned host in/w/out; H2D, kernels and D2H pipelined over 8 image chunks)"}
+
+    # ---- tensor-pipe peaks (after every timed GPU measurement), then the rooflines ---
+    mm_peaks = None
+    if rank == 0 and not args.no_extras:
+        mm_peaks = measure_matmul_peaks(dev)
+        PK.update(fp16=mm_peaks["fp16"]["burst_tflops"], tf32=mm_peaks["tf32"]["burst_tflops"], measured=True)
+        c_peak, c_peak_src = contraction_peak_of(gemm_name)
+        if "stage_ms" in extras.get("arm_3xtf32", {}):
+            a3 = extras["arm_3xtf32"]
+            pk3, pk3_src = contraction_peak_of("tcgen05_3xtf32")
+            a3["contraction"] = dict(stage_rooflines(a3.pop("_info"), a3["stage_ms"], 4, hbm_peak, pk3, cfg)[2],
+                                     peak_source=pk3_src)
+            a3["layer_roofline_frac"] = layer_roofline_frac(a3["contraction_info"], hbm_peak, pk3, a3["ms_rank"])
+    for a3 in (extras.get("arm_3xtf32", {}),):
+        a3.pop("_info", None)
+        a3.pop("contraction_info", None)
+        a3.pop("ms_rank", None)
     # ---- roofline of the dominant kernel ------------------------------------------
+    stages = stage_rooflines(info, stage_ms, nst, hbm_peak, c_peak, cfg)
+    dom = max(stages, key=lambda d: d["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            key = "%s/%s/m=%d" % (cfg.name, method, m)
+            ent = tj.get("%s/B=%d/%s" % (key, cfg.B, gemm_name)) or (tj.get(key) if cfg.B == base.B else None)
+            traffic = (ent or {}).get(dom["kernel"])
+        except Exception:
+            traffic = None
+    roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
+                "peak_source": ("%s: %s" % (peaks_src,
+                                            "HBM copy GB/s" if dom["bound"] == "hbm" else c_peak_src))}
+    layer_frac = layer_roofline_frac(info, hbm_peak, c_peak, ms_step if world == 1 else rank_ms) if nst == 4 else None
+
+    cpu = cpu_fp32 = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(base, args.cpu_baseline_s)
+        cpu_fp32 = cpu_direct_baseline(base, args.cpu_baseline_s)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+            "ms_per_step_stats": {"rank0_median": step_stats["median"], "rank0_min": step_stats["min"],
+                                  "rank0_max": step_stats["max"], "per_rank_ms": rank_ms_all,
+                                  "how": "CUDA events around each step of the timed region (rank 0)"},
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": base.name, "global_batch": gcfg.B, "B_per_gpu": cfg.B, "C": cfg.C,
+                       "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": method, "m": m,
+                       "t": info["t"], "gemm": gemm_name,
+                       "l2": ("flushed: 2x126 MB written between timed steps, steps timed alone "
+                              "(inputs+outputs %.0f MB/GPU < 2x L2)" % (io_bytes / 1e6)) if flush else
+                             ("no flush: inputs+outputs %.0f MB/GPU > 2x 126 MB L2" % (io_bytes / 1e6)),
+                       "parallelism": "dp%d (batch-sharded ranks of one global draw, no collective on the data "
+                                      "path, kernels transformed locally)" % world,
+                       "oversubscribed": oversub,
+                       "arith": ("fp32 storage; contraction %s with fp32 TMEM accumulation" % (
+                           "F16X3 (scaled fp16 hi/lo split, 3 products, kind::f16) on tcgen05"
+                           if gemm_name == "tcgen05_f16x3" else "3xTF32 on tcgen05"
+                           if gemm_name == "tcgen05_3xtf32" else "FFMA"))},
+            "roofline": roofline,
+            "layer_roofline_frac": layer_frac,
+            "stages": stages,
+            "sweep": sweep,
+            "planner": plan_report,
+            "matmul_peaks": mm_peaks,
+            "cpu_baseline": cpu,
+            "cpu_direct_fp32": cpu_fp32,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": plan.launches * args.steps * world,
+            "gpu_launches_per_rank": plan.launches * args.steps,
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    parallel.barrier()
+
+
+def stage_rooflines(info, stage_ms, nst, hbm_peak, c_peak, cfg):
     names = ["NK1 kernel transform", "NK2 input transform", "NK3 contraction", "NK4 output transform"]
     stages = []
     for s in range(nst):
@@ -409,127 +644,74 @@ def main():
             ach = cfg.direct_flops / tsec / 1e12
             stages.append({"kernel": "NK5 direct", "ms": stage_ms[s], "bound": "alu", "achieved": ach,
                            "peak": None, "unit": "TFLOP/s", "frac": None})
-    dom = max(stages, key=lambda d: d["ms"])
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            traffic = tj.get("%s/%s/m=%d" % (cfg.name, method, m), {}).get(dom["kernel"])
-        except Exception:
-            traffic = None
-    roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                "frac": dom["frac"], "traffic": traffic, "kernel": dom["kernel"],
-                "peak_source": ("%s: %s" % (peaks_src,
-                                            "HBM copy GB/s" if dom["bound"] == "hbm" else c_peak_src))}
-    # whole-layer roofline (paper Eq. running-time, stage sum)
+    return stages
+
+
+def layer_roofline_frac(info, hbm_peak, c_peak, ms):
+    """Whole-layer stage-sum roofline (paper Eq. running-time) / measured time."""
     t_roof = 0.0
-    if nst == 4:
-        for s in range(4):
-            tb = info["alg_bytes"][s] / (hbm_peak * 1e9)
-            tc = info["alg_flops"][s] / (c_peak * 1e12) if (s == 2 and c_peak) else 0.0
-            t_roof += max(tb, tc)
-    layer_frac = (t_roof * 1e3) / ms_step if t_roof else None
+    for s in range(4):
+        tb = info["alg_bytes"][s] / (hbm_peak * 1e9)
+        tc = info["alg_flops"][s] / (c_peak * 1e12) if (s == 2 and c_peak) else 0.0
+        t_roof += max(tb, tc)
+    return (t_roof * 1e3) / ms
 
+
+def run_extras(args, fc, cfg, plan, x, w, out, ws, stream, timer_fn, job_flops, world, dev, oversub, hbm_peak,
+               contraction_peak_of, method, m, parallel):
+    """Secondary measurements on the same rank-local layer and protocol: the 3xTF32 arm (the
+    north_star's arithmetic), inference with cached weight transforms, a CUDA-graph replay."""
+    import torch
+    red = dev if not oversub else None
+    res = {}
+    # ---- 3xTF32 contraction arm (same config, method, m and protocol) ------------------
+    try:
+        p3 = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, "tcgen05")
+        ws3 = p3.alloc_workspace(dev)
+        for _ in range(args.warmup):
+            p3.forward(x, w, out, ws3)
+        torch.cuda.synchronize()
+        parallel.barrier()
+        n3 = max(20, args.steps // 5)
+        t3, _ = timer_fn.run(n3, lambda: p3.forward(x, w, out, ws3))
+        ms3 = parallel.max_over_ranks(t3 / n3, red)
+        prof = [p3.forward_profiled(x, w, out, ws3) for _ in range(3)]
+        st3 = [min(p_[s] for p_ in prof) for s in range(4)]
+        # the contraction's roofline is filled in once the tensor peaks are measured (main())
+        res["arm_3xtf32"] = {"ms_per_step": ms3, "value": job_flops / (ms3 * 1e-3) / 1e12, "unit": UNIT,
+                             "method": method, "m": m, "stage_ms": [round(v, 4) for v in st3],
+                             "_info": p3.info, "contraction_info": p3.info, "ms_rank": t3 / n3}
+        del ws3, p3
+        torch.cuda.empty_cache()
+    except Exception as exc:  # reported, never fatal to the bench line
+        res["arm_3xtf32"] = {"error": str(exc)[:200]}
     # ---- inference with cached weight transforms (NK1 once, NK2-4 per call) -------
-    cached = None
-    if nst == 4:
-        ws_c = plan.alloc_workspace(dev)
-        plan.transform_weights(w, ws_c)
-        for _ in range(3):
-            plan.forward_cached(x, ws_c, out)
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        c0.record(stream)
-        nc = max(10, args.steps // 5)
-        for _ in range(nc):
-            plan.forward_cached(x, ws_c, out)
-        c1.record(stream)
-        torch.cuda.synchronize()
-        cms = parallel.max_over_ranks(c0.elapsed_time(c1) / nc, dev)
-        cached = {"ms_per_step": cms, "value": cfg.direct_flops * world / (cms * 1e-3) / 1e12, "unit": UNIT,
-                  "api": "conv_transform_weights once + conv_forward_cached (NK2-NK4) per step"}
-        del ws_c
-
+    ws_c = plan.alloc_workspace(dev)
+    plan.transform_weights(w, ws_c)
+    for _ in range(3):
+        plan.forward_cached(x, ws_c, out)
+    torch.cuda.synchronize()
+    nc = max(10, args.steps // 5)
+    tc_, _ = timer_fn.run(nc, lambda: plan.forward_cached(x, ws_c, out))
+    cms = parallel.max_over_ranks(tc_ / nc, red)
+    res["inference_cached_weights"] = {"ms_per_step": cms, "value": job_flops / (cms * 1e-3) / 1e12, "unit": UNIT,
+                                       "api": "conv_transform_weights once + conv_forward_cached (NK2-NK4) per step"}
+    del ws_c
     # ---- the same forward replayed as a CUDA graph of 10 steps (conv_graph_*) --------
-    graph = None
     try:
         gr = plan.capture(x, w, out, ws, steps=10)
         for _ in range(2):
             gr.launch(stream)
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        g0.record(stream)
         ng = max(5, args.steps // 10)
-        for _ in range(ng):
-            gr.launch(stream)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        gms = parallel.max_over_ranks(g0.elapsed_time(g1) / (10 * ng), dev)
-        graph = {"ms_per_step": gms, "value": cfg.direct_flops * world / (gms * 1e-3) / 1e12, "unit": UNIT,
-                 "api": "conv_graph_create(steps=10) once + conv_graph_launch per 10 steps"}
+        tg, _ = timer_fn.run(ng, lambda: gr.launch(stream))
+        gms = parallel.max_over_ranks(tg / (10 * ng), red)
+        res["cuda_graph"] = {"ms_per_step": gms, "value": job_flops / (gms * 1e-3) / 1e12, "unit": UNIT,
+                             "api": "conv_graph_create(steps=10) once + conv_graph_launch per 10 steps"}
         del gr
-    except Exception as exc:  # reported, never fatal to the bench line
-        graph = {"error": str(exc)[:200]}
-
-    # ---- end to end through the public API (host buffers, copies in the region) ---
-    e2e = None
-    if nst == 4 or True:
-        hi_, hw_ = I.pin_memory(), W.pin_memory()
-        ho_ = torch.empty(out.shape, dtype=torch.float32).pin_memory()
-        for _ in range(2):
-            plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
-        torch.cuda.synchronize()
-        parallel.barrier()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(args.e2e_steps):
-            plan.forward_host(hi_, hw_, ho_, x, w, out, ws)
-        s1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = parallel.max_over_ranks(s0.elapsed_time(s1) / args.e2e_steps, dev)
-        e2e = {"value": cfg.direct_flops * world / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": I.numel() * 4 + W.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
-               "api": "conv_forward_host (pinned host in/w/out; H2D, kernels and D2H pipelined over 8 image chunks)"}
-
-    cpu = cpu_fp32 = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_baseline_s)
-        cpu_fp32 = cpu_direct_baseline(cfg, args.cpu_baseline_s)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "ms_per_step_stats": {"rank0_median": step_stats["median"], "rank0_min": step_stats["min"],
-                                  "rank0_max": step_stats["max"],
-                                  "how": "CUDA events between consecutive steps of the timed region"},
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "B_per_gpu": cfg.B, "global_batch": cfg.B * world, "C": cfg.C,
-                       "l2_chunk_images": info.get("chunk"), "l2_chunks": info.get("nchunks"),
-                       "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": method, "m": m,
-                       "t": info["t"], "gemm": gemm_name,
-                       "l2": "no flush: inputs %.0f MB/GPU > 126 MB L2" % (I.numel() * 4 / 1e6),
-                       "parallelism": "dp%d (batch-sharded ranks, no collective on the data path)" % world,
-                       "arith": ("fp32 storage; contraction %s with fp32 TMEM accumulation" % (
-                           "F16X3 (scaled fp16 hi/lo split, 3 products, kind::f16) on tcgen05"
-                           if gemm_name == "tcgen05_f16x3" else "3xTF32 on tcgen05"
-                           if gemm_name == "tcgen05_3xtf32" else "FFMA"))},
-            "roofline": roofline,
-            "layer_roofline_frac": layer_frac,
-            "stages": stages,
-            "sweep": sweep,
-            "planner": plan_report,
-            "inference_cached_weights": cached,
-            "cuda_graph": graph,
-            "cpu_baseline": cpu,
-            "cpu_direct_fp32": cpu_fp32,
-            "clocks": clk,
-            "e2e": e2e,
-            "gpu_launches": plan.launches * args.steps,
-        }
-        print(json.dumps(line), flush=True)
-    parallel.barrier()
+    except Exception as exc:
+        res["cuda_graph"] = {"error": str(exc)[:200]}
+    return res
 
 
 if __name__ == "__main__":

@@ -67,8 +67,9 @@ typedef enum {
  *   F16X3   kind::f16 (2x the tf32 tensor rate): scaled fp16 splits
  *           a_hi = rn_f16(s a), a_lo = rn_f16(s a - a_hi) with exact power-of-two
  *           scales -- one per output channel c' for V (from max|W[c']| times the
- *           transform's norm bound, written by NK1) and one per forward for U
- *           (from max|U| reduced by NK2) -- removed again in the epilogue; the
+ *           transform's norm bound, written by NK1) and one per image b for U
+ *           (from max|U_b| reduced by NK2, so an image's result never depends on
+ *           the rest of its batch) -- removed again in the epilogue; the
  *           same 22 significant bits as 3xTF32 and no fp16 overflow by construction
  *           (reading R16). */
 typedef enum {
@@ -79,6 +80,33 @@ typedef enum {
 } conv_gemm_impl;
 
 typedef struct conv_plan_s *conv_plan_t;
+
+/* Plan options (conv_plan_opts / conv_plan_query_opts).  Every choice a plan makes
+ * is a function of (B, C, C', H, W, r, method, m) and these options only -- the
+ * library reads no environment variables.  Initialise with conv_plan_options_init()
+ * (the defaults are the measured-best settings) and override fields; a NULL options
+ * pointer means the defaults.  Invalid values -> CONV_ERR_INVALID_ARG. */
+typedef struct {
+    int struct_size;          /* sizeof(conv_plan_options), set by conv_plan_options_init */
+    conv_gemm_impl gemm;      /* contraction implementation (default CONV_GEMM_AUTO = F16X3) */
+    int gauss_combine;        /* Gauss-FFT with F16X3 and C' % 32 == 0: combine Re = T1 - T3,
+                                 Im = T1 + T2 in the contraction's epilogue (X at w = 2,
+                                 P:427-441).  -1 (default): the stage-sum model decides
+                                 (P:772-780); 0: never; 1: whenever eligible */
+    int complex_mode;         /* Regular-FFT with tcgen05, C' % 256 == 0, C % 16 (32 for F16X3)
+                                 == 0: store V as (V_r, V_i) planes and negate V_i in the MMA.
+                                 -1 (default): when eligible; 0: store the real embedding */
+    int chunk_images;         /* 0 (default): NK2 -> NK3 -> NK4 over the whole batch; k > 0:
+                                 in chunks of k images (L2-resident U / X; measured slower) */
+    int generic_transforms;   /* 0 (default): compile-time-t transform kernels where they
+                                 exist; 1: always the runtime-t kernels (reference / tests) */
+    int single_cta_mma;       /* 0 (default): CTA-pair contraction tiles when M > 128;
+                                 1: single-CTA tiles */
+    int e2e_chunks;           /* pipelining depth of conv_forward_host (0 = default 8) */
+} conv_plan_options;
+
+/* Fill `o` with the defaults (NULL-safe). */
+void conv_plan_options_init(conv_plan_options *o);
 
 /* Geometry and algorithmic cost of a plan (PAPER.md
  * Table "layer-stuff" P:1008-1042 with c = C, c' = C', alpha = 1). */
@@ -114,21 +142,45 @@ typedef struct {
                            X is then [E][2C'][BN_pad] like Regular-FFT's); 0 for CONV_DIRECT */
 } conv_plan_info;
 
-/* Host-only: validate arguments and fill `info` (no CUDA calls).  Errors:
- * INVALID_ARG if any size < 1, H < r, W < r, or m < 1 for a fast method;
- * UNSUPPORTED for Winograd with r < 2, m < 2 or t > 8, or FFT with t > 64. */
+/* Host-only: validate arguments and fill `info` (no CUDA calls).  m = 0 for a
+ * fast method selects the model's tile (conv_plan_best_m).  Errors:
+ * INVALID_ARG if any size < 1, H < r, W < r, or m < 0;
+ * UNSUPPORTED for Winograd with r < 2, m < 2 or t > 8, or FFT with t > 64.
+ * conv_plan_query reports CONV_GEMM_AUTO's plan; conv_plan_query_opts the plan
+ * `opts` (NULL = defaults) would build, e.g. for another contraction mode. */
 conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r,
                             conv_method method, int m, conv_plan_info *info);
+conv_status conv_plan_query_opts(int B, int C, int Cout, int H, int W, int r,
+                                 conv_method method, int m, const conv_plan_options *opts,
+                                 conv_plan_info *info);
+
+/* Host-only tile-size planner (the paper's comparison rule
+ * "each method at its best m"): for a fast method, evaluate the paper's
+ * stage-sum running-time model (per stage max(FLOPs / peak, bytes /
+ * bandwidth), summed) with B200 constants -- HBM 6.53 TB/s, the contraction
+ * mode's tensor ceiling, and per-kernel-family efficiencies measured on B200
+ * -- for every output tile m whose transforms are compiled
+ * (Winograd t <= 8; FFT t <= 32), and return the m of least predicted time
+ * (ties: the smaller m).  *m_out gets that m, *model_ms its predicted
+ * time (may be NULL).  n_cand / cand_m / cand_ms (may be NULL) receive up to
+ * max_cand (m, predicted ms) pairs in increasing m.  CONV_DIRECT -> INVALID_ARG. */
+conv_status conv_plan_best_m(int B, int C, int Cout, int H, int W, int r, conv_method method,
+                             const conv_plan_options *opts, int *m_out, double *model_ms,
+                             int max_cand, int *n_cand, int *cand_m, double *cand_ms);
 
 /* Create a plan on the current CUDA device, which must be sm_100 (B200; the library
  * carries sm_100a code only -- other devices get CONV_ERR_UNSUPPORTED) (uploads ~KB of constants:
  * Winograd matrices built exactly in rationals, DFT twiddles computed in fp64,
- * both rounded once to fp32).  m is ignored for CONV_DIRECT.  `*out` is set
- * only on CONV_OK; release with conv_destroy. */
+ * both rounded once to fp32).  m is ignored for CONV_DIRECT; m = 0 for a fast
+ * method takes conv_plan_best_m's tile (conv_plan_get_info reports it).  `*out`
+ * is set only on CONV_OK; release with conv_destroy.  conv_plan_ex(gemm) is
+ * conv_plan_opts with the defaults and that contraction mode. */
 conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
                       conv_method method, int m);
 conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
                          conv_method method, int m, conv_gemm_impl gemm);
+conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                           conv_method method, int m, const conv_plan_options *opts);
 
 conv_status conv_plan_get_info(conv_plan_t p, conv_plan_info *info);
 
@@ -148,8 +200,8 @@ conv_status conv_forward_profiled(conv_plan_t p, const float *in, const float *w
 
 /* End-to-end call with HOST buffers: copies h_in, h_w (pinned for overlap) to the
  * caller-provided device buffers d_in, d_w, runs the forward pass, copies d_out
- * back to h_out.  The batch is pipelined in image chunks (FASTCONV_E2E_CHUNKS,
- * default 8): H2D of chunk i+1, the kernels of chunk i and D2H of chunk i-1
+ * back to h_out.  The batch is pipelined in image chunks (
+ * conv_plan_options.e2e_chunks, default 8): H2D of chunk i+1, the kernels of chunk i and D2H of chunk i-1
  * overlap on plan-owned copy streams.  Asynchronous: when `stream` (the
  * caller's) completes, h_out holds the result (the caller synchronises). */
 conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w, float *h_out,
@@ -177,8 +229,8 @@ conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const floa
  * V_lo are fp32 (3XTF32 / FFMA) or fp16 (F16X3) [Z][M][Kp] planes. */
 conv_status conv_workspace_layout(conv_plan_t p, size_t offsets[4]);
 /* F16X3 plans: byte offsets of the per-output-channel scales (fp32 [2][C']:
- * s_v[c'] then 1/s_v[c'], exact powers of two) and of the max|U| word (fp32 bits)
- * inside the workspace; both 0 for other plans. */
+ * s_v[c'] then 1/s_v[c'], exact powers of two) and of the per-image max|U_b|
+ * words (fp32 bits, [chunk] of them) inside the workspace; both 0 for other plans. */
 conv_status conv_workspace_aux(conv_plan_t p, size_t offsets[2]);
 
 /* The plan's Winograd matrices in fp64 (exact rationals): AT [m][t], BT [t][t],

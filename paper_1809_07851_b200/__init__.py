@@ -36,6 +36,26 @@ class ConvError(RuntimeError):
         super().__init__("%s: %s" % (STATUS.get(status, status), detail))
 
 
+class PlanOptions(ctypes.Structure):
+    """conv_plan_options (include/fastconv.h): every plan choice besides the layer shape."""
+    _fields_ = [("struct_size", ctypes.c_int), ("gemm", ctypes.c_int), ("gauss_combine", ctypes.c_int),
+                ("complex_mode", ctypes.c_int), ("chunk_images", ctypes.c_int),
+                ("generic_transforms", ctypes.c_int), ("single_cta_mma", ctypes.c_int),
+                ("e2e_chunks", ctypes.c_int)]
+
+
+def options(gemm: str = "auto", **kw) -> PlanOptions:
+    """conv_plan_options_init() defaults, then ``gemm`` and any field given by name."""
+    o = PlanOptions()
+    load().conv_plan_options_init(ctypes.byref(o))
+    o.gemm = GEMMS[gemm]
+    for k, v in kw.items():
+        if k not in dict(PlanOptions._fields_):
+            raise TypeError("unknown plan option %r" % k)
+        setattr(o, k, int(v))
+    return o
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = ([(n, ctypes.c_int) for n in
                  ("B", "C", "Cout", "H", "W", "r", "m", "method", "Ho", "Wo", "t", "n_h", "n_w",
@@ -72,14 +92,19 @@ def load(build_if_missing: bool = False):
             raise RuntimeError("libfastconv.so is not built; run __graft_entry__.build() "
                                "(or python paper_1809_07851_b200/_build.py)")
         _build.build()
-    lib = ctypes.CDLL(os.environ.get("FASTCONV_LIB", _build.LIB))
+    lib = ctypes.CDLL(_build.LIB)
     vp, i, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
     dp = ctypes.POINTER(ctypes.c_double)
     fp = ctypes.POINTER(ctypes.c_float)
     sigs = {
         "conv_plan_query": ([i] * 8 + [ctypes.POINTER(PlanInfo)], i),
+        "conv_plan_query_opts": ([i] * 8 + [ctypes.POINTER(PlanOptions), ctypes.POINTER(PlanInfo)], i),
+        "conv_plan_options_init": ([ctypes.POINTER(PlanOptions)], None),
+        "conv_plan_best_m": ([i] * 7 + [ctypes.POINTER(PlanOptions), ctypes.POINTER(i), dp, i,
+                                        ctypes.POINTER(i), ctypes.POINTER(i), dp], i),
         "conv_plan": ([ctypes.POINTER(vp)] + [i] * 8, i),
         "conv_plan_ex": ([ctypes.POINTER(vp)] + [i] * 9, i),
+        "conv_plan_opts": ([ctypes.POINTER(vp)] + [i] * 8 + [ctypes.POINTER(PlanOptions)], i),
         "conv_plan_get_info": ([vp, ctypes.POINTER(PlanInfo)], i),
         "conv_workspace_bytes": ([vp], sz),
         "conv_forward": ([vp, vp, vp, vp, vp, sz, vp], i),
@@ -125,10 +150,28 @@ def _check(st: int):
         raise ConvError(st, load().conv_last_error().decode())
 
 
-def plan_query(B, C, Cout, H, W, r, method: str, m: int = 0) -> dict:
+def plan_query(B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto", **opts) -> dict:
+    """conv_plan_query_opts: the geometry and algorithmic costs of the plan these options build
+    (m = 0: the planner's tile)."""
     info = PlanInfo()
-    _check(load().conv_plan_query(B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(info)))
+    o = options(gemm, **opts)
+    _check(load().conv_plan_query_opts(B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o), ctypes.byref(info)))
     return info.as_dict()
+
+
+def best_m(B, C, Cout, H, W, r, method: str, gemm: str = "auto", **opts):
+    """conv_plan_best_m: (m, predicted ms, {m: predicted ms}) from the paper's stage-sum model
+    with B200 constants, over every compiled tile size."""
+    o = options(gemm, **opts)
+    m = ctypes.c_int()
+    ms = ctypes.c_double()
+    cap = 64
+    n = ctypes.c_int()
+    cm = (ctypes.c_int * cap)()
+    cms = (ctypes.c_double * cap)()
+    _check(load().conv_plan_best_m(B, C, Cout, H, W, r, METHODS[method], ctypes.byref(o), ctypes.byref(m),
+                                   ctypes.byref(ms), cap, ctypes.byref(n), cm, cms))
+    return m.value, ms.value, {cm[k]: cms[k] for k in range(n.value)}
 
 
 def winograd_matrices(m: int, r: int):
@@ -149,6 +192,10 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream)
 
 
+def _nbytes(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size()
+
+
 def _check_tensor(x: torch.Tensor, name: str, shape=None):
     if not isinstance(x, torch.Tensor):
         raise TypeError("%s must be a torch.Tensor" % name)
@@ -165,10 +212,11 @@ def _check_tensor(x: torch.Tensor, name: str, shape=None):
 class Plan:
     """conv_plan(B, C, C', H, W, r, method, m) -- immutable; owns only host metadata + constants."""
 
-    def __init__(self, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto"):
+    def __init__(self, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto", **opts):
         lib = load()
         h = ctypes.c_void_p()
-        _check(lib.conv_plan_ex(ctypes.byref(h), B, C, Cout, H, W, r, METHODS[method], m, GEMMS[gemm]))
+        o = options(gemm, **opts)
+        _check(lib.conv_plan_opts(ctypes.byref(h), B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o)))
         self._h = h
         self.method = method
         info = PlanInfo()
@@ -206,14 +254,14 @@ class Plan:
         if workspace is None:
             workspace = self.alloc_workspace(x.device)
         _check(load().conv_forward(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                   workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                   workspace.data_ptr(), _nbytes(workspace),
                                    _stream_ptr(stream)))
         return out
 
     def transform_weights(self, w, workspace, stream=None):
         """NK1 once into the workspace's V region (conv_transform_weights)."""
         _check_tensor(w, "weights", self.w_shape)
-        _check(load().conv_transform_weights(self._h, w.data_ptr(), workspace.data_ptr(), workspace.numel(),
+        _check(load().conv_transform_weights(self._h, w.data_ptr(), workspace.data_ptr(), _nbytes(workspace),
                                              _stream_ptr(stream)))
 
     def forward_cached(self, x, workspace, out=None, stream=None) -> torch.Tensor:
@@ -223,13 +271,13 @@ class Plan:
             out = torch.empty(self.out_shape, dtype=torch.float32, device=x.device)
         _check_tensor(out, "out", self.out_shape)
         _check(load().conv_forward_cached(self._h, x.data_ptr(), out.data_ptr(), workspace.data_ptr(),
-                                          workspace.numel(), _stream_ptr(stream)))
+                                          _nbytes(workspace), _stream_ptr(stream)))
         return out
 
     def forward_profiled(self, x, w, out, workspace, stream=None):
         ms = (ctypes.c_float * 4)()
         _check(load().conv_forward_profiled(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                            workspace.data_ptr(), workspace.numel(), _stream_ptr(stream), ms))
+                                            workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream), ms))
         return list(ms)
 
     def forward_host(self, h_in, h_w, h_out, d_in, d_w, d_out, workspace, stream=None):
@@ -239,12 +287,12 @@ class Plan:
                 raise ValueError("%s must be a contiguous float32 host tensor" % n)
         _check(load().conv_forward_host(self._h, h_in.data_ptr(), h_w.data_ptr(), h_out.data_ptr(),
                                         d_in.data_ptr(), d_w.data_ptr(), d_out.data_ptr(),
-                                        workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+                                        workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream)))
 
     def run_stage(self, stage: int, x=None, w=None, out=None, workspace=None, stream=None):
         p = lambda t_: 0 if t_ is None else t_.data_ptr()
         _check(load().conv_run_stage(self._h, stage, p(x), p(w), p(out), workspace.data_ptr(),
-                                     workspace.numel(), _stream_ptr(stream)))
+                                     _nbytes(workspace), _stream_ptr(stream)))
 
     def capture(self, x, w, out, workspace, steps: int = 1, cached: bool = False) -> "Graph":
         """conv_graph_create: `steps` forwards on these fixed buffers as one CUDA graph."""
@@ -254,7 +302,7 @@ class Plan:
             _check_tensor(w, "weights", self.w_shape)
         h = ctypes.c_void_p()
         _check(load().conv_graph_create(self._h, x.data_ptr(), 0 if cached else w.data_ptr(), out.data_ptr(),
-                                        workspace.data_ptr(), workspace.numel(), int(steps), int(bool(cached)),
+                                        workspace.data_ptr(), _nbytes(workspace), int(steps), int(bool(cached)),
                                         ctypes.byref(h)))
         return Graph(h, (self, x, w, out, workspace))
 
@@ -295,7 +343,7 @@ class StageTimer:
 
     def forward(self, plan: "Plan", x, w, out, workspace, stream=None):
         _check(load().conv_forward_timed(plan._h, x.data_ptr(), w.data_ptr(), out.data_ptr(),
-                                         workspace.data_ptr(), workspace.numel(), _stream_ptr(stream),
+                                         workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream),
                                          self._h))
 
     def read(self):
@@ -314,12 +362,22 @@ class StageTimer:
             self._h = None
 
 
+_PLAN_CACHE: dict = {}
+_PLAN_CACHE_MAX = 32
+
+
 def forward(x: torch.Tensor, w: torch.Tensor, method: str = "winograd", m: int = 4,
             gemm: str = "auto") -> torch.Tensor:
-    """One-shot forward: plans, allocates workspace/output with torch, runs on the current stream."""
+    """One-shot forward: plans (cached by shape, method, m, gemm and device), allocates the
+    workspace and output with torch, runs on the current stream.  m = 0: the planner's tile."""
     B, C, H, W = x.shape
     Cout, C2, r, _ = w.shape
     if C2 != C:
         raise ValueError("channel mismatch")
-    plan = Plan(B, C, Cout, H, W, r, method, m, gemm)
+    key = (B, C, Cout, H, W, r, method, m, gemm, x.device.index if x.is_cuda else -1)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        if len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+        plan = _PLAN_CACHE[key] = Plan(B, C, Cout, H, W, r, method, m, gemm)
     return plan.forward(x, w)

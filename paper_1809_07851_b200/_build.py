@@ -34,18 +34,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (one nvcc per translation unit), then
+    link the shared library."""
     if not force and not _stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC] + NVCC_FLAGS + ["-o", tmp] + sources()
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((src, obj, [NVCC] + compile_flags + ["-c", "-o", obj, src]))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs))
     log = os.path.join(PKG, "build.log")
+    tmp = LIB + ".tmp"
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp] + \
+        [j[1] for j in jobs] + ["-lcuda"] * 0
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        for (src, obj, cmd), res in zip(jobs, results):
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        bad = [(j, r) for j, r in zip(jobs, results) if r.returncode != 0]
+        if bad:
+            raise RuntimeError("nvcc failed (see %s):\n%s" % (log, "\n".join(r.stderr[-3000:] for _, r in bad)))
+        res = subprocess.run(link, capture_output=True, text=True)
+        f.write(" ".join(link) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed (see %s):\n%s" % (log, res.stderr[-4000:]))
+        raise RuntimeError("link failed (see %s):\n%s" % (log, res.stderr[-4000:]))
     if verbose:
-        print(res.stderr)
+        print("".join(r.stderr for r in results))
     os.replace(tmp, LIB)
     return LIB
 

@@ -186,9 +186,6 @@ int fc_max_clusters(const void *func, const cudaLaunchConfig_t *cfg) {
         n = 0;
     }
     cache[{func, dev}] = n;
-    if (getenv("FASTCONV_DEBUG_CLUSTERS"))
-        fprintf(stderr, "fastconv: kernel %p cluster %d x %d threads, %zu B smem: %d co-resident clusters\n", func,
-                cfg->numAttrs ? (int)cfg->attrs[0].val.clusterDim.x : 1, (int)cfg->blockDim.x, cfg->dynamicSmemBytes, n);
     return n;
 }
 
@@ -207,23 +204,14 @@ Geometry fc_chunk_geometry(const Geometry &g, int Bc) {
     return c;
 }
 
-// Optional L2-resident batch chunking: images per chunk so that a chunk's U + X
-// (+ V) could stay in L2 between NK2 -> NK3 -> NK4 (B200: 126 MB L2); among
-// near-maximal chunk sizes prefer the one whose B*N fills whole 256-wide
-// contraction tiles.  OFF by default: on VGG-3.2 (F(4,3)) chunks of 2/4/6/8
-// images measured 2.5x / 1.7x / 1.5x / 1.4x slower than one pass (smaller
-// launches pay wave tails and partial contraction tiles; profiles/r01_notes.md).
-// FASTCONV_CHUNK=<images> forces a chunk size (0 = whole batch);
-// FASTCONV_L2_BUDGET_MB=<MB> enables the budget heuristic.
 // Gauss epilogue combine: it saves one of X's three planes in NK3's writes and
 // NK4's reads, but three accumulators fit TMEM only as 128-column tiles, and those run the
 // F16X3 contraction ~1.35x slower per FLOP than 256-column tiles (per-SM operand traffic:
 // V' is re-staged per 128 columns).  Decide by the paper's stage-sum model for
 // NK3 + NK4 with B200 constants measured on this kernel set (profiles/r01_summary.md);
-// FASTCONV_GC=0/1 forces the choice.  G: Z, K, E, BN filled, Gauss-FFT.
-static bool gauss_combine_pays(const Geometry &G) {
-    const char *env = getenv("FASTCONV_GC");
-    if (env) return atoi(env) != 0;
+// conv_plan_options.gauss_combine forces the choice.  G: Z, K, E, BN filled, Gauss-FFT.
+static bool gauss_combine_pays(const Geometry &G, int force) {
+    if (force >= 0) return force != 0;
     const double bw = 6.5e12, bw4 = 4.9e12;     // HBM: streaming / NK4's achieved
     const double r256 = 1.3e15, r128 = 0.95e15;  // F16X3 issue rate (3 fp16 products / FLOP)
     const double BN = (double)G.BN, E = G.E, C = G.C, Co = G.Cout;
@@ -238,36 +226,121 @@ static bool gauss_combine_pays(const Geometry &G) {
     return tgc < t3;
 }
 
-static int pick_chunk(const Geometry &G, size_t bytes_V) {
-    if (G.method == CONV_DIRECT) return G.B;
-    const char *env = getenv("FASTCONV_CHUNK");
-    if (env) {
-        const int c = atoi(env);
-        return (c <= 0 || c > G.B) ? G.B : c;
+// Optional batch chunking (conv_plan_options.chunk_images): NK2 -> NK3 -> NK4 per group of
+// images so that a chunk's U and X could stay in the 126 MB L2.  Off by default: on VGG-3.2
+// (F(4,3)) chunks of 2/4/6/8 images measured 2.5x / 1.7x / 1.5x / 1.4x slower than one pass
+// (smaller launches pay wave tails and partial contraction tiles; profiles/r01_summary.md).
+static int pick_chunk(const Geometry &G, int chunk_images) {
+    if (G.method == CONV_DIRECT || chunk_images <= 0 || chunk_images > G.B) return G.B;
+    return chunk_images;
+}
+
+static conv_status check_options(const conv_plan_options *o) {
+    if (o->struct_size != (int)sizeof(conv_plan_options)) {
+        fc_set_error("conv_plan_options.struct_size is %d, expected %d (use conv_plan_options_init)", o->struct_size,
+                     (int)sizeof(conv_plan_options));
+        return CONV_ERR_INVALID_ARG;
     }
-    const char *benv = getenv("FASTCONV_L2_BUDGET_MB");
-    if (!benv) return G.B;
-    const double budget = atof(benv) * 1e6;
-    const double per_img = 4.0 * ((double)G.Z * G.K + (double)G.Xz * G.Xm) * G.N;
-    const double avail = budget - (double)bytes_V;
-    long long bmax = avail > per_img ? (long long)(avail / per_img) : 1;
-    if (bmax >= G.B) return G.B;
-    if (bmax < 1) bmax = 1;
-    int best = (int)bmax;
-    double best_eff = 0.0;
-    for (long long bc = bmax; bc >= 1 && bc * 4 >= bmax * 3; --bc) {
-        const double cols = (double)bc * G.N;
-        const double eff = cols / (std::ceil(cols / 256.0) * 256.0);
-        if (eff > best_eff + 1e-9) {
-            best_eff = eff;
-            best = (int)bc;
+    if (o->gemm < CONV_GEMM_AUTO || o->gemm > CONV_GEMM_TCGEN05_F16X3) {
+        fc_set_error("unknown gemm implementation %d", (int)o->gemm);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (o->gauss_combine < -1 || o->gauss_combine > 1 || o->complex_mode < -1 || o->complex_mode > 1 ||
+        o->chunk_images < 0 || o->generic_transforms < 0 || o->generic_transforms > 1 || o->single_cta_mma < 0 ||
+        o->single_cta_mma > 1 || o->e2e_chunks < 0) {
+        fc_set_error("conv_plan_options field out of range");
+        return CONV_ERR_INVALID_ARG;
+    }
+    return CONV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Tile-size planner: the paper's running-time model -- each stage
+// bound by its compute or its memory traffic, stages summed -- with B200's
+// measured HBM bandwidth and the contraction mode's tensor ceiling (MEASURED_PEAKS.json:
+// 6534.5 GB/s, dense fp16/bf16 1634 TFLOP/s -> F16X3 545 and 3xTF32 272 fp32-equivalent
+// TFLOP/s, three products per fp32 product; FFMA 74 TFLOP/s = 148 SMs x 128 lanes x 2 x
+// 1.965 GHz).  Each stage's time is divided by the fraction of its roofline this kernel
+// family reaches on B200 (kModelEff, measured over BASELINE.json's configs; DESIGN.md
+// section 7), and the contraction's tensor work counts the padded columns it really issues.
+// ---------------------------------------------------------------------------
+namespace {
+struct ModelEff {
+    double nk1, nk2, nk3, nk4;
+};
+// Winograd / FFT transform families (measured fraction of the stage roofline, B200)
+constexpr ModelEff kEffWino = {0.50, 0.88, 0.88, 0.86};
+constexpr ModelEff kEffFft = {0.50, 0.75, 0.85, 0.70};
+}  // namespace
+
+double fc_model_ms(const conv_plan_info &I, const Geometry &G) {
+    const double bw = 6534.5e9;
+    const int gemm = I.gemm;
+    const double peak = gemm == CONV_GEMM_TCGEN05_F16X3 ? 1634.2e12 / 3.0
+                        : gemm == CONV_GEMM_TCGEN05_3XTF32 ? 0.5 * 1634.2e12 / 3.0 : 74.4e12;
+    const ModelEff &ef = G.method == CONV_WINOGRAD ? kEffWino : kEffFft;
+    const double eff[4] = {ef.nk1, ef.nk2, ef.nk3, ef.nk4};
+    double t = 0.0;
+    for (int s = 0; s < 4; ++s) {
+        double ts = I.alg_bytes[s] / bw;
+        if (s == 2) {  // tensor work on the padded columns (N = 128 / 256 tiles)
+            const double pad = I.BN > 0 ? (double)I.BN_pad / (double)I.BN : 1.0;
+            ts = std::max(ts, I.alg_flops[2] * pad / peak);
+        }
+        t += ts / eff[s];
+    }
+    return t * 1e3;
+}
+
+conv_status fc_best_m(int B, int C, int Cout, int H, int W, int r, int method, const conv_plan_options *opts,
+                      int *m_out, double *model_ms, int max_cand, int *n_cand, int *cand_m, double *cand_ms) {
+    if (method != CONV_WINOGRAD && method != CONV_REGULAR_FFT && method != CONV_GAUSS_FFT) {
+        fc_set_error("conv_plan_best_m: method %d has no tile size", method);
+        return CONV_ERR_INVALID_ARG;
+    }
+    const int tmax = method == CONV_WINOGRAD ? 8 : 32;
+    int best = 0, nc = 0;
+    double best_t = 0.0;
+    conv_status last = CONV_ERR_UNSUPPORTED;
+    for (int m = 1; m + r - 1 <= tmax; ++m) {
+        if (!fc_fast_transforms(method, m + r - 1, m, r)) continue;
+        Geometry g;
+        conv_plan_info I;
+        conv_status st = fc_fill_geometry(B, C, Cout, H, W, r, method, m, &g, &I, opts);
+        if (st != CONV_OK) {
+            last = st;
+            continue;
+        }
+        if (I.gemm == CONV_GEMM_AUTO) I.gemm = CONV_GEMM_TCGEN05_F16X3;
+        const double t = fc_model_ms(I, g);
+        if (cand_m && cand_ms && nc < max_cand) {
+            cand_m[nc] = m;
+            cand_ms[nc] = t;
+        }
+        ++nc;
+        if (!best || t < best_t) {  // strict: ties keep the smaller m
+            best = m;
+            best_t = t;
         }
     }
-    return best;
+    if (n_cand) *n_cand = nc < max_cand ? nc : max_cand;
+    if (!best) {
+        if (last == CONV_ERR_UNSUPPORTED)
+            fc_set_error("conv_plan_best_m: no compiled tile size for method %d with r = %d", method, r);
+        return last;
+    }
+    *m_out = best;
+    if (model_ms) *model_ms = best_t;
+    return CONV_OK;
 }
 
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
-                             Geometry *g, conv_plan_info *info, conv_gemm_impl gemm) {
+                             Geometry *g, conv_plan_info *info, const conv_plan_options *opts) {
+    {
+        conv_status st = check_options(opts);
+        if (st != CONV_OK) return st;
+    }
+    const conv_gemm_impl gemm = opts->gemm;
     if (B < 1 || C < 1 || Cout < 1 || H < 1 || W < 1 || r < 1) {
         fc_set_error("sizes must be >= 1 (B=%d C=%d C'=%d H=%d W=%d r=%d)", B, C, Cout, H, W, r);
         return CONV_ERR_INVALID_ARG;
@@ -280,13 +353,13 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         fc_set_error("unknown method %d", method);
         return CONV_ERR_INVALID_ARG;
     }
-    if (method != CONV_DIRECT && m < 1) {
-        fc_set_error("output tile m must be >= 1 (got %d)", m);
+    if (method != CONV_DIRECT && m < 0) {
+        fc_set_error("output tile m must be >= 1, or 0 for the planner's choice (got %d)", m);
         return CONV_ERR_INVALID_ARG;
     }
-    if (gemm < CONV_GEMM_AUTO || gemm > CONV_GEMM_TCGEN05_F16X3) {
-        fc_set_error("unknown gemm implementation %d", (int)gemm);
-        return CONV_ERR_INVALID_ARG;
+    if (method != CONV_DIRECT && m == 0) {  // the planner's tile (conv_plan_best_m)
+        conv_status st = fc_best_m(B, C, Cout, H, W, r, method, opts, &m, nullptr, 0, nullptr, nullptr, nullptr);
+        if (st != CONV_OK) return st;
     }
     if ((long long)B * C * H * W >= (1LL << 40) || (long long)Cout * C * r * r >= (1LL << 40)) {
         fc_set_error("tensor too large");
@@ -334,16 +407,17 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
         const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
         G.Kp = (G.K + kq - 1) / kq * kq;
-        G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G);
+        G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G, opts->gauss_combine);
         G.Xz = G.gc ? G.E : G.Z;
         G.Xm = G.gc ? 2 * Cout : G.M;
         G.cplx = 0;
         if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % (G.vf16 ? 32 : 16) == 0 &&
-            !getenv("FASTCONV_NO_CPLX")) {
+            opts->complex_mode != 0) {
             G.cplx = 1;
             G.Kp = (C + kq - 1) / kq * kq;
         }
     }
+    G.tc_1sm = opts->single_cta_mma;
     *g = G;
     if (info) {
         conv_plan_info I;
@@ -361,9 +435,9 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
             const int split = (gemm != CONV_GEMM_FFMA);
             const size_t vb = fc_v_bytes(G);  // V_hi, then V_lo at the next 256 B boundary
             I.bytes_V = split ? align256(vb) + vb : vb;
-            if (G.vf16)  // + per-c' scales [2][C'] and the max|U| word
-                I.bytes_V = align256(I.bytes_V) + align256((size_t)2 * Cout * 4) + 256;
-            I.chunk = pick_chunk(G, I.bytes_V);
+            I.chunk = pick_chunk(G, opts->chunk_images);
+            if (G.vf16)  // + per-c' scales [2][C'] and the per-image max|U_b| words of a chunk
+                I.bytes_V = align256(I.bytes_V) + align256((size_t)2 * Cout * 4) + align256((size_t)I.chunk * 4);
             I.nchunks = (B + I.chunk - 1) / I.chunk;
             const Geometry Gc = fc_chunk_geometry(G, I.chunk);
             I.BN_pad = Gc.BN_pad;
@@ -415,10 +489,47 @@ const char *conv_status_string(conv_status s) {
 
 const char *conv_last_error(void) { return g_err; }
 
+void conv_plan_options_init(conv_plan_options *o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->struct_size = (int)sizeof(conv_plan_options);
+    o->gemm = CONV_GEMM_AUTO;
+    o->gauss_combine = -1;
+    o->complex_mode = -1;
+    o->chunk_images = 0;
+    o->generic_transforms = 0;
+    o->single_cta_mma = 0;
+    o->e2e_chunks = 0;
+}
+
+static const conv_plan_options *opts_or_default(const conv_plan_options *o, conv_plan_options *tmp) {
+    if (o) return o;
+    conv_plan_options_init(tmp);
+    return tmp;
+}
+
+conv_status conv_plan_query_opts(int B, int C, int Cout, int H, int W, int r, conv_method method, int m,
+                                 const conv_plan_options *opts, conv_plan_info *info) {
+    conv_plan_options d;
+    Geometry g;
+    return fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &g, info, opts_or_default(opts, &d));
+}
+
 conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r, conv_method method, int m,
                             conv_plan_info *info) {
-    Geometry g;
-    return fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &g, info, CONV_GEMM_AUTO);
+    return conv_plan_query_opts(B, C, Cout, H, W, r, method, m, nullptr, info);
+}
+
+conv_status conv_plan_best_m(int B, int C, int Cout, int H, int W, int r, conv_method method,
+                             const conv_plan_options *opts, int *m_out, double *model_ms, int max_cand, int *n_cand,
+                             int *cand_m, double *cand_ms) {
+    if (!m_out || max_cand < 0) {
+        fc_set_error("conv_plan_best_m: NULL m_out or negative max_cand");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_plan_options d;
+    return fc_best_m(B, C, Cout, H, W, r, (int)method, opts_or_default(opts, &d), m_out, model_ms, max_cand, n_cand,
+                     cand_m, cand_ms);
 }
 
 conv_status conv_winograd_matrices(int m, int r, double *AT, double *BT, double *G) {
@@ -429,21 +540,31 @@ conv_status conv_winograd_matrices(int m, int r, double *AT, double *BT, double 
     return fc_winograd_rational(m, r, AT, BT, G);
 }
 
-conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
-                         conv_method method, int m, conv_gemm_impl gemm) {
+conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                           conv_method method, int m, const conv_plan_options *opts_in) {
     if (!out) {
         fc_set_error("NULL plan pointer");
         return CONV_ERR_INVALID_ARG;
     }
+    conv_plan_options opts;
+    if (opts_in) {
+        conv_status st = check_options(opts_in);
+        if (st != CONV_OK) return st;
+        opts = *opts_in;
+    } else {
+        conv_plan_options_init(&opts);
+    }
     conv_plan_s *p = (conv_plan_s *)calloc(1, sizeof(conv_plan_s));
     if (!p) return CONV_ERR_OUT_OF_MEMORY;
+    conv_gemm_impl gemm = opts.gemm;
     if (gemm == CONV_GEMM_AUTO) gemm = fc_tcgen05_available() ? CONV_GEMM_TCGEN05_F16X3 : CONV_GEMM_FFMA;
     if ((gemm == CONV_GEMM_TCGEN05_3XTF32 || gemm == CONV_GEMM_TCGEN05_F16X3) && !fc_tcgen05_available()) {
         free(p);
         fc_set_error("tcgen05 contraction not available in this build");
         return CONV_ERR_UNSUPPORTED;
     }
-    conv_status st = fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &p->g, &p->info, gemm);
+    opts.gemm = gemm;
+    conv_status st = fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &p->g, &p->info, &opts);
     if (st != CONV_OK) { free(p); return st; }
     p->gemm = gemm;
     const Geometry &g = p->g;
@@ -472,7 +593,7 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
             cc.sinv[j] = (float)sin(ang);
         }
     }
-    p->generic_transforms = getenv("FASTCONV_GENERIC_TRANSFORMS") != nullptr;
+    p->generic_transforms = opts.generic_transforms;
     cudaError_t e = cudaGetDevice(&p->device);
     if (e != cudaSuccess) {
         fc_set_error("cudaGetDevice: %s", cudaGetErrorString(e));
@@ -523,11 +644,7 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
     }
     p->chunk = p->info.chunk;
     p->nchunks = p->info.nchunks;
-    {
-        const char *ev = getenv("FASTCONV_E2E_CHUNKS");
-        p->e2e_chunks = ev ? atoi(ev) : 8;
-        if (p->e2e_chunks < 1) p->e2e_chunks = 1;
-    }
+    p->e2e_chunks = opts.e2e_chunks > 0 ? opts.e2e_chunks : 8;
     if (method != CONV_DIRECT && p->e2e_chunks > 1) {  // copy streams for the pipelined host path
         if (cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking) != cudaSuccess) {
@@ -540,9 +657,17 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
     return CONV_OK;
 }
 
+conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                         conv_method method, int m, conv_gemm_impl gemm) {
+    conv_plan_options o;
+    conv_plan_options_init(&o);
+    o.gemm = gemm;
+    return conv_plan_opts(out, B, C, Cout, H, W, r, method, m, &o);
+}
+
 conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
                       conv_method method, int m) {
-    return conv_plan_ex(out, B, C, Cout, H, W, r, method, m, CONV_GEMM_AUTO);
+    return conv_plan_opts(out, B, C, Cout, H, W, r, method, m, nullptr);
 }
 
 void conv_destroy(conv_plan_t p) {
@@ -691,7 +816,8 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, cons
         }
         case 1: {
             if (g.vf16) {  // NK2 reduces max|U| for the contraction's fp16 scale
-                conv_status st = launch_result(cudaMemsetAsync(g.umax, 0, sizeof(unsigned int), s), "max|U| reset");
+                conv_status st = launch_result(cudaMemsetAsync(g.umax, 0, sizeof(unsigned int) * (size_t)g.B, s),
+                                               "max|U_b| reset");
                 if (st) return st;
             }
             int handled = 0;

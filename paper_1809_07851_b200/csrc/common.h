@@ -64,11 +64,13 @@ struct Geometry {
                   // embedding; the contraction picks the plane per K-half and negates -V_i
     // F16X3 contraction (conv_gemm_impl CONV_GEMM_TCGEN05_F16X3): V_hi / V_lo are fp16,
     // Kp = K rounded up to 8 (16-byte rows), scaled per output channel c' by
-    // vscale[c'] = 2^k (inverse at vscale[Cout + c']); NK2 reduces max|U| into *umax
-    // (fp32 bits, reset before every NK2).  Pointers are filled per call (workspace).
+    // vscale[c'] = 2^k (inverse at vscale[Cout + c']); NK2 reduces max|U| of every image b
+    // into umax[b] (fp32 bits, [B] words, reset before every NK2), and the contraction scales
+    // the columns of image b by s_u[b] = 2^(15 - e), max|U_b| < 2^e.  Pointers are filled per
+    // call (workspace).
     int vf16;
     float vbound;            // host bound: max|V[.][c'][.]| <= vbound * max|W[c']|
-    unsigned int *umax;      // NK2 -> NK3 (nullptr: NK2 does not reduce)
+    unsigned int *umax;      // [B] per-image max|U|, NK2 -> NK3 (nullptr: NK2 does not reduce)
     float *vscale;           // [2][Cout]: NK1 writes, NK3 epilogue reads the inverse
     FastDiv divN, divNw;     // n -> (image, tile) and tile -> (row, column) in the transforms
     // X = [Xz][Xm][BN_pad]: Xz = Z, Xm = M, except the Gauss epilogue combine (gc = 1:
@@ -76,6 +78,7 @@ struct Geometry {
     // as rows [0, C') / [C', 2C') of Xz = E planes -- the Regular-FFT layout
     // ("X at w = 2")
     int gc, Xz, Xm;
+    int tc_1sm;  // conv_plan_options.single_cta_mma: single-CTA contraction tiles even when M > 128
 };
 
 struct conv_plan_s {
@@ -87,7 +90,7 @@ struct conv_plan_s {
     ConvConsts *d_consts;                 // device copy
     int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
-    size_t off_vscale, off_umax;          // F16X3: per-c' scales [2][Cout], max|U| word (else 0)
+    size_t off_vscale, off_umax;          // F16X3: per-c' scales [2][Cout], per-image max|U| [B] (else 0)
     int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
     int e2e_chunks;                       // pipelining depth of conv_forward_host
     cudaStream_t h2d, d2h;                // copy streams of the pipelined host path
@@ -112,18 +115,29 @@ inline size_t fc_v_floats(const Geometry &g) {
 }
 inline size_t fc_v_bytes(const Geometry &g) { return fc_v_floats(g) * (g.vf16 ? 2 : 4); }
 
-// Block-wide max of non-negative floats into *gmax (fp32 bit patterns order as
-// unsigned integers): warp reduce, shared atomic, one global atomic per CTA.
-// Every thread of the block must call it (no early returns before).
+// F16X3 per-image max|U| (the contraction's U scale is per image, so an image's arithmetic
+// never depends on the other images of its batch, chunk or shard): every thread of the block
+// calls this once with its image b (b < 0: no contribution) and its non-negative max v.  Lanes
+// of one image are combined in the warp, warps through shared slots for the 32 images starting
+// at b0 (the image of the CTA's first tile), then one global atomicMax per (CTA, image) into
+// umax[b] (fp32 bit patterns of non-negative floats order as unsigned integers).  Images
+// outside the 32 slots fall back to one global atomic per warp.  No early returns before it.
 #ifdef __CUDACC__
-__device__ __forceinline__ void fc_block_umax(unsigned int *gmax, float v) {
-    __shared__ unsigned int s_max;
-    if (threadIdx.x == 0) s_max = 0u;
+__device__ __forceinline__ void fc_block_umax_img(unsigned int *umax, int b0, int b, float v) {
+    __shared__ unsigned int s_max[32];
+    if (threadIdx.x < 32) s_max[threadIdx.x] = 0u;
     __syncthreads();
-    const unsigned int u = __reduce_max_sync(0xffffffffu, __float_as_uint(v));
-    if ((threadIdx.x & 31) == 0) atomicMax(&s_max, u);
+    const unsigned int grp = __match_any_sync(0xffffffffu, b);
+    const unsigned int u = __reduce_max_sync(grp, __float_as_uint(v));
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1) && b >= 0 && u) {
+        const int slot = b - b0;
+        if (slot >= 0 && slot < 32)
+            atomicMax(&s_max[slot], u);
+        else
+            atomicMax(umax + b, u);
+    }
     __syncthreads();
-    if (threadIdx.x == 0 && s_max) atomicMax(gmax, s_max);
+    if (threadIdx.x < 32 && s_max[threadIdx.x]) atomicMax(umax + b0 + threadIdx.x, s_max[threadIdx.x]);
 }
 // Store one transformed-kernel value V[o]: split 0 = fp32; 1 = 3xTF32 pair
 // (hi = rna_tf32(v), lo = v - hi, fp32); 2 = F16X3 pair of scaled fp16
@@ -228,9 +242,16 @@ int fc_num_sms();
 // the current device -- a persistent clustered grid larger than this runs in two waves
 // (cached per (kernel, device); 0 if the query fails)
 int fc_max_clusters(const void *func, const cudaLaunchConfig_t *cfg);
+// opts: resolved options (never NULL; opts->gemm may be CONV_GEMM_AUTO for queries)
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
-                             Geometry *g, conv_plan_info *info, conv_gemm_impl gemm);
+                             Geometry *g, conv_plan_info *info, const conv_plan_options *opts);
 conv_status fc_winograd_rational(int m, int r, double *AT, double *BT, double *G);
+// planner (conv_plan_best_m): the stage-sum model's ms for a filled plan, and the best m
+double fc_model_ms(const conv_plan_info &I, const Geometry &G);
+conv_status fc_best_m(int B, int C, int Cout, int H, int W, int r, int method, const conv_plan_options *opts,
+                      int *m_out, double *model_ms, int max_cand, int *n_cand, int *cand_m, double *cand_ms);
+// 1 when (method, t, m, r) has compile-time-t NK2 / NK4 kernels (transforms_fast.cu)
+int fc_fast_transforms(int method, int t, int m, int r);
 void fc_set_error(const char *fmt, ...);
 
 // ---- kernel launchers (return cudaGetLastError()) ----

@@ -442,9 +442,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // output, read from HBM once per tile) and the four splitter warps write
 // U'_hi = rn_f16(s_u U), U'_lo = rn_f16(s_u U - U'_hi) K-major in the same
 // 64 B-swizzled layout (row = tile column n, 16-byte chunk = 8 K values).
-// s_u = 2^(15 - e) with max|U| < 2^e (NK2's reduction), so |s_u U| < 2^15 and
-// no fp16 overflows; the epilogue multiplies each accumulator row by
-// 1 / (s_u s_v[c']) (exact powers of two) before the TMA store of X.
+// s_u = s_u[b] = 2^(15 - e) with max|U_b| < 2^e over image b's tiles (NK2's per-image
+// reduction), so |s_u U| < 2^15 and no fp16 overflows, and an image's arithmetic does
+// not depend on the rest of its batch; the epilogue multiplies accumulator (c', n) by
+// 1 / (s_u[b(n)] s_v[c']) (exact powers of two) before the TMA store of X.
 template <int CG, int BLOCK_N, int SA, int SU, bool GC = false>
 struct TcCfgF16 {
     // GC (Gauss epilogue combine): the three products T1, T2, T3 of one (e, c', n) tile
@@ -480,7 +481,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     nk3_gemm_tcgen05_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                          const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, int M,
                          int K, long long NP, int Z, int cplx, int Mh, int kb_half, int Cout,
-                         const unsigned int *__restrict__ umax_p, const float *__restrict__ inv_sv) {
+                         const unsigned int *__restrict__ umax_p, const float *__restrict__ inv_sv, FastDiv divN,
+                         int BNr) {
     using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU, GC>;
     using I = Tc<CG>;
     constexpr int BK = Cfg::BK, NACC = Cfg::NACC, SUB = Cfg::SUB;
@@ -542,6 +544,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         m0 = mb * Cfg::BM;
         n0 = (rest % n_n) * BLOCK_N;
         z = rest / n_n;
+    };
+    // per-image U scale s_u[b] = 2^(15 - e), max|U_b| < 2^e (NK2's per-image reduction);
+    // column n < BNr belongs to image n / N (padding columns: image 0, their X is never read)
+    auto col_scale = [&](int col) {
+        return fc_pow2_scale(__uint_as_float(umax_p[col < BNr ? fc_div(col, divN) : 0]), 15);
     };
 
     if (warp == 0) {
@@ -649,7 +656,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // of plane e; unscaled as above; two 32 x 32 boxes per chunk
         const int q = warp & 3;
         const uint32_t stage0 = epi0 + q * (4 * 4096);
-        const float inv_su = 1.f / fc_pow2_scale(__uint_as_float(*umax_p), 15);
         int acc = 0, buf = 0;
         uint32_t acc_phase = 0;
         for (int T = grp; T < num_tiles; T += ngrp) {
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             decode(T, e, m0, n0);
             const int row0 = m0 + 128 * (int)rank + q * 32;
             const int cp = row0 + lane;
-            const float rs = cp < Cout ? inv_su * __ldg(inv_sv + cp) : 0.f;
+            const float rs = cp < Cout ? __ldg(inv_sv + cp) : 0.f;
             int a[3];
 #pragma unroll
             for (int p = 0; p < 3; ++p) {  // the three slots of this tile, in issue order
@@ -673,6 +679,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
             for (int c = 0; c < BLOCK_N / 32; ++c) {
                 uint32_t v1[32], v2[32], v3[32];
+                const float inv_col = 1.f / col_scale(n0 + 32 * c + lane);  // lane = column here
                 const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16) + c * 32;
                 TMEM_LD_32(tl + a[0] * BLOCK_N, v1);
                 TMEM_LD_32(tl + a[1] * BLOCK_N, v2);
@@ -687,8 +694,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const float t1 = __uint_as_float(v1[4 * j + i]);
-                        re[i] = (t1 - __uint_as_float(v3[4 * j + i])) * rs;
-                        im[i] = (t1 + __uint_as_float(v2[4 * j + i])) * rs;
+                        const float sc = rs * __shfl_sync(0xffffffffu, inv_col, 4 * j + i);
+                        re[i] = (t1 - __uint_as_float(v3[4 * j + i])) * sc;
+                        im[i] = (t1 + __uint_as_float(v2[4 * j + i])) * sc;
                     }
                     const uint32_t o = lane * 128 + ((j ^ (lane & 7)) << 4);
                     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sre + o), "f"(re[0]), "f"(re[1]),
@@ -728,7 +736,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ---- epilogue: unscale by 1 / (s_u s_v[c']) and TMA-store X (as the tf32 kernel)
         const int q = warp & 3;
         const uint32_t stage0 = epi0 + q * (2 * 4096);
-        const float inv_su = 1.f / fc_pow2_scale(__uint_as_float(*umax_p), 15);
         int acc = 0, buf = 0;
         uint32_t acc_phase = 0;
         for (int T = grp; T < num_tiles; T += ngrp) {
@@ -737,19 +744,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int row0 = m0 + 128 * (int)rank + q * 32;
             int cp = row0 + lane;
             cp = cp >= Cout ? cp - Cout : cp;  // rows [C', 2C') of the Regular-FFT products: Im of c'
-            const float rs = cp < Cout ? inv_su * __ldg(inv_sv + cp) : 0.f;
+            const float rs = cp < Cout ? __ldg(inv_sv + cp) : 0.f;
             mbar_wait(tfull_bar(acc), acc_phase);
             tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BLOCK_N / 32; ++c) {
                 uint32_t v[32];
+                const float inv_col = 1.f / col_scale(n0 + 32 * c + lane);  // lane = column here
                 const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BLOCK_N + c * 32;
                 TMEM_LD_32(taddr, v);
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 __syncwarp();
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * rs);
+                for (int j = 0; j < 32; ++j)
+                    v[j] = __float_as_uint(__uint_as_float(v[j]) * (rs * __shfl_sync(0xffffffffu, inv_col, j)));
                 const uint32_t sb = stage0 + buf * 4096;
                 const uint32_t rowaddr = sb + lane * 128;
 #pragma unroll
@@ -781,10 +790,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (warp >= 8) {
         // ---- splitter: fp32 U [BK][NH] -> scaled fp16 (hi, lo), K-major 64 B-swizzled rows
         const int st = threadIdx.x - 256;
-        const float su_scale = fc_pow2_scale(__uint_as_float(*umax_p), 15);
+        static_assert(128 % Cfg::NH == 0, "a splitter thread converts one tile column n = st % NH");
+        const int ncol = st % Cfg::NH;
         int sa = 0, su = 0;
         uint32_t pa = 0, pu = 0;
-        for (int T = grp; T < num_tiles; T += ngrp)
+        for (int T = grp; T < num_tiles; T += ngrp) {
+        int z0_, m0_, n0_;
+        decode(T, z0_, m0_, n0_);
+        const float su_scale = col_scale(n0_ + (int)rank * Cfg::NH + ncol);  // this column's image
         for (int p = 0; p < SUB; ++p) {
             for (int kb = 0; kb < num_k; ++kb) {
                 mbar_wait(fullU_bar(su), pu);
@@ -795,7 +808,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < Cfg::NH * BK / 8 / 128; ++i) {
                     const int chunk = st + 128 * i;
-                    const int n = chunk % Cfg::NH, kg = chunk / Cfg::NH;  // 8 K values kg*8.. of column n
+                    const int n = ncol, kg = chunk / Cfg::NH;  // 8 K values kg*8.. of column n
                     float x[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) x[j] = uf[(kg * 8 + j) * Cfg::NH + n] * su_scale;
@@ -826,6 +839,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     pu ^= 1;
                 }
             }
+        }
         }
     }
 
@@ -984,7 +998,11 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
     if (g.cplx && (g.Cout % Cfg::BM != 0 || g.C % Cfg::BK != 0)) return cudaErrorInvalidValue;
     const unsigned int *um = g.umax;
     const float *isv = g.vscale + g.Cout;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mU, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, Cout_, um, isv);
+    if (g.BN >= (1LL << 31)) return cudaErrorInvalidValue;
+    const FastDiv dN = g.divN;
+    const int BNr = (int)g.BN;
+    cudaError_t e =
+        cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mU, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, Cout_, um, isv, dN, BNr);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -996,7 +1014,7 @@ int fc_tcgen05_available() { return get_encode() != nullptr; }
 cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                                    cudaStream_t s) {
     if (!Vlo) return cudaErrorInvalidValue;
-    static const int force_1cta = getenv("FASTCONV_TC_1SM") != nullptr;
+    const int force_1cta = g.tc_1sm;
     // M > 128: CTA pairs (M = 256 per MMA); M <= 128: single CTAs (M = 128 per MMA)
     if (g.M > 128 && !force_1cta) return launch<2, 256, 6, 16>(g, Vhi, Vlo, U, X, s);
     return launch<1, 256, 4, 16>(g, Vhi, Vlo, U, X, s);
@@ -1005,7 +1023,7 @@ cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const fl
 cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const void *Vlo, const float *U, float *X,
                                        cudaStream_t s) {
     if (!Vlo || !g.umax || !g.vscale) return cudaErrorInvalidValue;
-    static const int force_1cta = getenv("FASTCONV_TC_1SM") != nullptr;
+    const int force_1cta = g.tc_1sm;
     // rings (operand stages, fp32 U stages): 4/4 measured 163 us vs 3/6 170 us on VGG-3.2 F(4,3)
     if (g.gc) {  // Gauss epilogue combine: 4 accumulator slots of 128 columns
         if (g.M > 128 && !force_1cta) return launch_f16<2, 128, 5, 4, true>(g, Vhi, Vlo, U, X, s);

@@ -178,8 +178,12 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
         }
     }
     __syncthreads();
-    // column pass along the H axis and store; nn fastest for coalescing
-    float umx = 0.f;
+    // column pass along the H axis and store; nn fastest for coalescing.  F16X3: per-tile
+    // max|U| in shared slots (s_d is free after the row pass), then per image in global
+    unsigned int *s_tmax = reinterpret_cast<unsigned int *>(s_d);
+    if (g.umax)
+        for (int i = threadIdx.x; i < TN; i += blockDim.x) s_tmax[i] = 0u;
+    __syncthreads();
     for (int idx = threadIdx.x; idx < TN * E; idx += blockDim.x) {
         const int nn = idx % TN, e = idx / TN;
         const long long n = n0 + nn;
@@ -205,16 +209,20 @@ __global__ void __launch_bounds__(256) nk2_input_transform(Geometry g, const Con
                 U[fc_u_off(g, n, c, E + e)] = ar;
                 U[fc_u_off(g, n, c, 2 * E + e)] = ai;
             }
-            umx = fmaxf(umx, fabsf(ar) + fabsf(ai));
+            if (g.umax) atomicMax(s_tmax + nn, __float_as_uint(fabsf(ar) + fabsf(ai)));
         } else {
             float a = 0.f;
             const float *zc = s_z + (size_t)nn * t * t + l;
             for (int aa = 0; aa < t; ++aa) a = fmaf(s_BT[k * t + aa], zc[aa * t], a);
             U[fc_u_off(g, n, c, e)] = a;
-            umx = fmaxf(umx, fabsf(a));
+            if (g.umax) atomicMax(s_tmax + nn, __float_as_uint(fabsf(a)));
         }
     }
-    if (g.umax) fc_block_umax(g.umax, umx);
+    if (g.umax) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < TN; i += blockDim.x)
+            if (n0 + i < g.BN && s_tmax[i]) atomicMax(g.umax + (n0 + i) / g.N, s_tmax[i]);
+    }
 }
 
 // ---------------------------------------------------------------- NK4 ------

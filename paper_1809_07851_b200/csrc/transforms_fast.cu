@@ -22,6 +22,14 @@
 
 using fct::cf;
 
+// FFT tile edges t with compile-time NK1 / NK2 / NK4 codelets (mixed-radix products of
+// 2, 3, 5, 7 and the primes 13 and 31 up to 32; "arbitrary sizes").
+#define FC_FFT_TILES(X)                                                                                    \
+    X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(13) X(14) X(15) X(16) X(18) X(20) X(21) X(24) X(25) X(27) \
+        X(28) X(30) X(31) X(32)
+// (t, m) Winograd pairs with compile-time matrices
+#define FC_WINO_TILES(X) X(4, 2) X(4, 3) X(5, 3) X(6, 4) X(6, 2) X(8, 6)
+
 namespace {
 
 struct WinoMats {
@@ -186,7 +194,10 @@ __global__ void __launch_bounds__(RED ? 128 : 512, (RED && T <= 6) ? 8 : (RED ? 
             dp += zs;
             if (RED) umx = fmaxf(umx, fabsf(s));
         }
-    if (RED) fc_block_umax(g.umax, umx);
+    if (RED) {  // per-image max|U| (b0: the image of the CTA's first tile)
+        const long long nf = (long long)(cfast ? blockIdx.y : blockIdx.x) * blockDim.x;
+        fc_block_umax_img(g.umax, fc_div((int)(nf < g.BN ? nf : g.BN - 1), g.divN), b, umx);
+    }
 }
 
 
@@ -614,7 +625,11 @@ __global__ void __launch_bounds__(256, ((T <= 16 && T % 2 == 0) || T == 9) ? 5 :
             }
         }
     }
-    if (g.umax) fc_block_umax(g.umax, umx);
+    if (g.umax) {  // per-image max|U|: a thread's items all have tile nn = threadIdx.x % FTN
+        const long long nt = n0 + (threadIdx.x % FTN);
+        fc_block_umax_img(g.umax, fc_div((int)(n0 < g.BN ? n0 : g.BN - 1), g.divN),
+                          nt < g.BN ? fc_div((int)nt, g.divN) : -1, umx);
+    }
 }
 
 // ---------------------------------------------------------------- FFT NK4 ---
@@ -725,15 +740,14 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
     if (forward) {
         const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
         fc_smem_attr((const void *)nk2_fft<T>, (int)smem);
-        static const int cf = getenv("FASTCONV_NK2F_NFAST") ? 0 : 1;  // channel-fastest grid (measured faster)
-        static const int v2_env = getenv("FASTCONV_NK2_NOV2") ? 0 : 1;
-        const int v2 = (v2_env && ((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
+        // channel-fastest grid (measured faster); float2 row loads when tile rows are 8-byte aligned
+        const int v2 = (((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
         // small tiles (t <= 12): CTAs of exactly max(row pairs, columns) x 32 threads -- one
         // item each, no idle warps (VGG-3.2 t = 10 NK2 -7%, deep t = 9 -6%); larger tiles keep
         // 256 (t = 16 at 288 threads: one CTA fewer per SM, VGG-1.2 m = 14 +5%)
         constexpr int RPc = (T + 1) / 2, ITEMS = (RPc > H ? RPc : H) * FTN;
         const int nthr = (T <= 12 && ITEMS <= 256) ? (ITEMS + 31) / 32 * 32 : 256;
-        if (cf && nblk <= 65535)
+        if (nblk <= 65535)
             nk2_fft<T><<<dim3(g.C, nblk), nthr, smem, s>>>(g, src, dst, 1 | v2);
         else
             nk2_fft<T><<<dim3(nblk, g.C), nthr, smem, s>>>(g, src, dst, v2);
@@ -745,7 +759,7 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         auto smem_of = [&](int ipc, int r) {
             return (size_t)ipc * r * g.n_w * Sm * sizeof(float2) + (size_t)ipc * r * g.m * SWo * sizeof(float);
         };
-        static const int items_env = getenv("FASTCONV_NK4F_ITEMS") ? atoi(getenv("FASTCONV_NK4F_ITEMS")) : 256;
+        constexpr int items_env = 256;
         // at least 32 tiles per CTA: each (l, c') run of X a warp loads is then >= 128 bytes
         // (VGG-1.2 m = 14 had 16-tile strips: 64-byte runs)
         const int target = items_env / H > 32 ? items_env / H : 32;
@@ -770,20 +784,10 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
     return cudaGetLastError();
 }
 
-// ------------------------------------------- Winograd NK2 / NK4, plane pipeline ---
-// Whole (b, c) image planes (NK2) or whole per-plane X columns (NK4) are streamed
-// into shared memory with 1-D TMA bulk copies (cp.async.bulk + mbarrier
-// complete_tx) through an NSLOT-deep ring, so the next planes' loads are in
-// flight while the CTA transforms the current one (the thread-per-tile kernels
-// above keep only a few scattered 4-byte loads per thread in flight).  A CTA
-// loops over groups of G planes (G x N tiles ~ one tile per thread):
-//   NK2  group = (b, channels c0..c0+G-1): one contiguous copy of G H x W planes;
-//        thread per tile computes U = B^T d B from smem (zero outside the image)
-//        and stores the t^2 values along n (coalesced 4-byte lanes).
-//   NK4  group = (c', images b0..b0+G-1): E copies of the G*N contiguous values
-//        X[e][c'][b0 N ...]; thread per tile computes Y = A^T X A and stores its
-//        m x m block straight into the output plane (float4 / float2 rows).
-constexpr int PLANE_SLOTS = 3;
+// ------------------------------------------------- TMA bulk-copy helpers ---
+// (A TMA plane-pipeline Winograd NK2 / NK4 -- whole image planes streamed into a 3-slot
+// shared-memory ring with cp.async.bulk -- measured slower than the thread-per-tile kernels
+// on VGG-3.2 F(4,3), NK2 178 vs 150 us, NK4 145 vs 133 us, and was removed in round 2.)
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -806,231 +810,6 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
         : "memory");
 }
 
-template <int T, bool RED>
-__global__ void __launch_bounds__(256) nk2_wino_plane(Geometry g, const float *__restrict__ in,
-                                                     float *__restrict__ U, int G) {
-    constexpr wtab::Tables tb = wtab::make(2, T - 1);
-    extern __shared__ float4 plane_smem4[];
-    float *sm = reinterpret_cast<float *>(plane_smem4);
-    __shared__ __align__(8) uint64_t bars[PLANE_SLOTS];
-    const int HW = g.H * g.W;
-    const int gpb = (g.C + G - 1) / G;  // channel groups per image
-    const int total = g.B * gpb;
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(bars);
-    auto issue = [&](int q, int slot) {
-        const int b = q / gpb, c0 = (q - b * gpb) * G;
-        const int ng = min(G, g.C - c0);
-        const uint32_t bytes = (uint32_t)ng * HW * 4u;
-        mbar_expect(bbase + 8 * slot, bytes);
-        bulk_g2s(sbase + (uint32_t)slot * G * HW * 4u, in + ((size_t)b * g.C + c0) * HW, bytes, bbase + 8 * slot);
-    };
-    if (threadIdx.x == 0) {
-        for (int sl = 0; sl < PLANE_SLOTS; ++sl) mbar_init1(bbase + 8 * sl);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int sl = 0; sl < PLANE_SLOTS; ++sl) {
-            const int q = blockIdx.x + sl * gridDim.x;
-            if (q < total) issue(q, sl);
-        }
-    }
-    __syncthreads();
-    const size_t estride = (size_t)g.K * g.BN_pad;
-    float umx = 0.f;
-    for (int k = 0;; ++k) {
-        const int q = blockIdx.x + k * gridDim.x;
-        if (q >= total) break;
-        const int slot = k % PLANE_SLOTS;
-        mbar_wait_parity(bbase + 8 * slot, (uint32_t)(k / PLANE_SLOTS) & 1u);
-        const int b = q / gpb, c0 = (q - b * gpb) * G;
-        const int ng = min(G, g.C - c0);
-        const float *sp = sm + (size_t)slot * G * HW;
-        for (int it = threadIdx.x; it < ng * g.N; it += blockDim.x) {
-            const int gi = it / g.N, tile = it - gi * g.N;
-            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
-            const int y0 = ti * g.m, x0 = tj * g.m;
-            const float *src = sp + gi * HW + y0 * g.W + x0;
-            float d[T][T];
-            if (y0 + T <= g.H && x0 + T <= g.W) {
-#pragma unroll
-                for (int a = 0; a < T; ++a)
-#pragma unroll
-                    for (int qq = 0; qq < T; ++qq) d[a][qq] = src[a * g.W + qq];
-            } else {
-#pragma unroll
-                for (int a = 0; a < T; ++a)
-#pragma unroll
-                    for (int qq = 0; qq < T; ++qq)
-                        d[a][qq] = (y0 + a < g.H && x0 + qq < g.W) ? src[a * g.W + qq] : 0.f;
-            }
-            float z[T][T];
-#pragma unroll
-            for (int a = 0; a < T; ++a)
-#pragma unroll
-                for (int l = 0; l < T; ++l) {
-                    float acc = -0.f;
-#pragma unroll
-                    for (int qq = 0; qq < T; ++qq) acc = wtab::cfma(tb.BT[l][qq], d[a][qq], acc);
-                    z[a][l] = acc;
-                }
-            float *dp = U + fc_u_off(g, (long long)b * g.N + tile, c0 + gi, 0);
-#pragma unroll
-            for (int kk = 0; kk < T; ++kk)
-#pragma unroll
-                for (int l = 0; l < T; ++l) {
-                    float acc = -0.f;
-#pragma unroll
-                    for (int a = 0; a < T; ++a) acc = wtab::cfma(tb.BT[kk][a], z[a][l], acc);
-                    dp[(kk * T + l) * fc_u_zs(g)] = acc;
-                    if (RED) umx = fmaxf(umx, fabsf(acc));
-                }
-        }
-        __syncthreads();  // every thread is done with the slot
-        if (threadIdx.x == 0) {
-            const int q2 = blockIdx.x + (k + PLANE_SLOTS) * gridDim.x;
-            if (q2 < total) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(q2, slot);
-            }
-        }
-    }
-    if (RED) fc_block_umax(g.umax, umx);
-}
-
-template <int T, int MM>
-__global__ void __launch_bounds__(256) nk4_wino_plane(Geometry g, const float *__restrict__ X,
-                                                     float *__restrict__ out, int G) {
-    constexpr wtab::Tables ta = wtab::make(MM, T - MM + 1);  // A^T as literals
-    constexpr int E = T * T;
-    extern __shared__ float4 plane_smem4[];
-    float *sm = reinterpret_cast<float *>(plane_smem4);
-    __shared__ __align__(8) uint64_t bars[PLANE_SLOTS];
-    const int gpc = (g.B + G - 1) / G;  // image groups per output channel
-    const int total = g.Cout * gpc;
-    const int GN = G * g.N;
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
-    const uint32_t bbase = (uint32_t)__cvta_generic_to_shared(bars);
-    const size_t estride = (size_t)g.Xm * g.BN_pad;
-    auto issue = [&](int q, int slot) {  // warp 0: lane j copies elements e = j, j + 32, ...
-        const int co = q / gpc, b0 = (q - co * gpc) * G;
-        const int ng = min(G, g.B - b0);
-        const uint32_t bytes = (uint32_t)ng * g.N * 4u;
-        if (threadIdx.x == 0) mbar_expect(bbase + 8 * slot, bytes * E);
-        __syncwarp();
-        const float *src = X + (size_t)co * g.BN_pad + (size_t)b0 * g.N;
-        for (int e = threadIdx.x; e < E; e += 32)
-            bulk_g2s(sbase + ((uint32_t)slot * E * GN + (uint32_t)e * GN) * 4u, src + e * estride, bytes,
-                     bbase + 8 * slot);
-    };
-    if (threadIdx.x == 0) {
-        for (int sl = 0; sl < PLANE_SLOTS; ++sl) mbar_init1(bbase + 8 * sl);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x < 32)
-        for (int sl = 0; sl < PLANE_SLOTS; ++sl) {
-            const int q = blockIdx.x + sl * gridDim.x;
-            if (q < total) issue(q, sl);
-        }
-    const int vec = (MM % 4 == 0 && g.Wo % 4 == 0) ? 4 : ((MM % 2 == 0 && g.Wo % 2 == 0) ? 2 : 1);
-    for (int k = 0;; ++k) {
-        const int q = blockIdx.x + k * gridDim.x;
-        if (q >= total) break;
-        const int slot = k % PLANE_SLOTS;
-        mbar_wait_parity(bbase + 8 * slot, (uint32_t)(k / PLANE_SLOTS) & 1u);
-        const int co = q / gpc, b0 = (q - co * gpc) * G;
-        const int ng = min(G, g.B - b0);
-        const float *sp = sm + (size_t)slot * E * GN;
-        for (int it = threadIdx.x; it < ng * g.N; it += blockDim.x) {
-            const int gi = it / g.N, tile = it - gi * g.N;
-            float y[MM][MM];
-            wino_out_tile<T, MM>(
-                [&](int k, float *x) {
-#pragma unroll
-                    for (int l = 0; l < T; ++l) x[l] = sp[(k * T + l) * GN + it];
-                },
-                y);
-            const int ti = tile / g.n_w, tj = tile - ti * g.n_w;
-            const int oy = ti * MM, ox = tj * MM;
-            float *op = out + (((size_t)(b0 + gi) * g.Cout + co) * g.Ho + oy) * g.Wo + ox;
-            const bool full_w = ox + MM <= g.Wo;
-#pragma unroll
-            for (int a = 0; a < MM; ++a) {
-                if (oy + a >= g.Ho) break;
-                float *rp = op + (size_t)a * g.Wo;
-                if (full_w && vec == 4) {
-#pragma unroll
-                    for (int qq = 0; qq < MM; qq += 4)
-                        __stcs(reinterpret_cast<float4 *>(rp + qq),
-                               make_float4(y[a][qq], y[a][(qq + 1) % MM], y[a][(qq + 2) % MM], y[a][(qq + 3) % MM]));
-                } else if (full_w && vec == 2) {
-#pragma unroll
-                    for (int qq = 0; qq < MM; qq += 2)
-                        __stcs(reinterpret_cast<float2 *>(rp + qq), make_float2(y[a][qq], y[a][(qq + 1) % MM]));
-                } else {
-#pragma unroll
-                    for (int qq = 0; qq < MM; ++qq)
-                        if (ox + qq < g.Wo) __stcs(rp + qq, y[a][qq]);
-                }
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int q2 = blockIdx.x + (k + PLANE_SLOTS) * gridDim.x;
-            if (q2 < total) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(q2, slot);
-            }
-        }
-    }
-}
-
-int sm_count() { return fc_num_sms(); }
-
-// plane-pipeline launchers: return false when the geometry does not qualify
-template <int T, int MM>
-bool launch_wino_plane(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s,
-                       cudaError_t *err) {
-    // opt-in (FASTCONV_PLANE=1): on VGG-3.2 F(4,3) it measured NK2 178 us / NK4 145 us
-    // against 150 / 133 us for the thread-per-tile kernels (profiles/r01_summary.md)
-    const bool on = getenv("FASTCONV_PLANE") != nullptr;  // read per launch (tests toggle it)
-    if (!on) return false;
-    const int HW = g.H * g.W;
-    if (forward) {
-        if (HW % 4 != 0 || (size_t)HW * 4 > 48 * 1024) return false;
-        int G = 256 / g.N;
-        G = G < 1 ? 1 : (G > g.C ? g.C : G);
-        while (G > 1 && (size_t)G * HW * 4 > 48 * 1024) --G;
-        const size_t smem = (size_t)PLANE_SLOTS * G * HW * 4;
-        const int per_sm = (int)((200 * 1024) / (smem + 1024)) < 4 ? (int)((200 * 1024) / (smem + 1024)) : 4;
-        const long long total = (long long)g.B * ((g.C + G - 1) / G);
-        long long grid = (long long)sm_count() * (per_sm < 1 ? 1 : per_sm);
-        if (grid > total) grid = total;
-        if (g.umax) {
-            fc_smem_attr((const void *)nk2_wino_plane<T, true>, 200 * 1024);
-            nk2_wino_plane<T, true><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
-        } else {
-            fc_smem_attr((const void *)nk2_wino_plane<T, false>, 200 * 1024);
-            nk2_wino_plane<T, false><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
-        }
-    } else {
-        const int E = T * T;
-        if (g.N % 4 != 0 || (size_t)E * g.N * 4 > 64 * 1024) return false;
-        int G = 256 / g.N;
-        G = G < 1 ? 1 : (G > g.B ? g.B : G);
-        while (G > 1 && (size_t)E * G * g.N * 4 > 48 * 1024) --G;
-        const size_t smem = (size_t)PLANE_SLOTS * E * G * g.N * 4;
-        int per_sm = (int)((200 * 1024) / (smem + 1024));
-        per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
-        const long long total = (long long)g.Cout * ((g.B + G - 1) / G);
-        long long grid = (long long)sm_count() * per_sm;
-        if (grid > total) grid = total;
-        fc_smem_attr((const void *)nk4_wino_plane<T, MM>, 200 * 1024);
-        nk4_wino_plane<T, MM><<<(unsigned)grid, 256, smem, s>>>(g, src, dst, G);
-    }
-    *err = cudaGetLastError();
-    return true;
-}
-
 // tile rows per CTA: the staged strip stays within ~32 KB of shared memory
 inline int wino_strip_rows(const Geometry &g, int row_floats) {
     const int per_tile_row = g.m * row_floats * 4;
@@ -1043,23 +822,20 @@ inline int wino_strip_rows(const Geometry &g, int row_floats) {
 
 template <int T, int MM>
 cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
-    cudaError_t perr = cudaSuccess;
-    if (launch_wino_plane<T, MM>(g, src, dst, forward, s, &perr)) return perr;
     if (forward) {
         {
-            static const int bs = getenv("FASTCONV_NK2_BS") ? atoi(getenv("FASTCONV_NK2_BS")) : 128;
-            static const int cf_env = getenv("FASTCONV_NK2_NFAST") ? 0 : 1;
-            static const int v2_env = getenv("FASTCONV_NK2_NOV2") ? 0 : 1;
-            const int v2 = (v2_env && ((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
+            // 128-tile CTAs (one U block), channel-fastest grid (measured faster than n-fastest)
+            constexpr int bs = FC_TB;
+            const int v2 = (((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
             if (g.umax) {
                 const unsigned nblk = (unsigned)((g.BN + 127) / 128);
-                if (cf_env && nblk <= 65535)
+                if (nblk <= 65535)
                     nk2_wino<T, true><<<dim3(g.C, nblk), 128, 0, s>>>(g, src, dst, 1 | v2);
                 else
                     nk2_wino<T, true><<<dim3(nblk, g.C), 128, 0, s>>>(g, src, dst, v2);
             } else {
                 const unsigned nblk = (unsigned)((g.BN + bs - 1) / bs);
-                if (cf_env && bs == FC_TB && nblk <= 65535)
+                if (nblk <= 65535)
                     nk2_wino<T, false><<<dim3(g.C, nblk), bs, 0, s>>>(g, src, dst, 1 | v2);
                 else
                     nk2_wino<T, false><<<dim3(nblk, g.C), bs, 0, s>>>(g, src, dst, v2);
@@ -1068,7 +844,7 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
     } else {
         // about 256 tiles per CTA: strips of one image, or several whole images
         const int SWo = g.n_w * g.m;
-        static const int target = getenv("FASTCONV_NK4_TILES") ? atoi(getenv("FASTCONV_NK4_TILES")) : 256;
+        constexpr int target = 256;
         int R = wino_strip_rows(g, SWo), IPC = 1;
         if (R * g.n_w > target) R = target / g.n_w > 0 ? target / g.n_w : 1;
         if (R >= g.n_h) {
@@ -1096,22 +872,17 @@ cudaError_t dispatch(const Geometry &g, const ConvConsts &hc, const float *src, 
     if (g.method == CONV_WINOGRAD) {
         (void)hc;
         // (t, m) pairs with compile-time matrices; others use the runtime-matrix kernels
-        if (g.t == 4 && g.m == 2) return launch_wino<4, 2>(g, src, dst, forward, s);
-        if (g.t == 4 && g.m == 3) return launch_wino<4, 3>(g, src, dst, forward, s);
-        if (g.t == 5 && g.m == 3) return launch_wino<5, 3>(g, src, dst, forward, s);
-        if (g.t == 6 && g.m == 4) return launch_wino<6, 4>(g, src, dst, forward, s);
-        if (g.t == 6 && g.m == 2) return launch_wino<6, 2>(g, src, dst, forward, s);
-        if (g.t == 8 && g.m == 6) return launch_wino<8, 6>(g, src, dst, forward, s);
+#define FC_WINO_CASE(TT, MM) \
+    if (g.t == TT && g.m == MM) return launch_wino<TT, MM>(g, src, dst, forward, s);
+        FC_WINO_TILES(FC_WINO_CASE)
+#undef FC_WINO_CASE
         *handled = false;
         return cudaSuccess;
     }
     switch (g.t) {
 #define FC_FFT_CASE(TT) \
     case TT: return launch_fft<TT>(g, src, dst, forward, s);
-        FC_FFT_CASE(4) FC_FFT_CASE(5) FC_FFT_CASE(6) FC_FFT_CASE(7) FC_FFT_CASE(8) FC_FFT_CASE(9)
-        FC_FFT_CASE(10) FC_FFT_CASE(12) FC_FFT_CASE(13) FC_FFT_CASE(14) FC_FFT_CASE(15) FC_FFT_CASE(16)
-        FC_FFT_CASE(18) FC_FFT_CASE(20) FC_FFT_CASE(21) FC_FFT_CASE(24) FC_FFT_CASE(25) FC_FFT_CASE(27)
-        FC_FFT_CASE(28) FC_FFT_CASE(30) FC_FFT_CASE(31) FC_FFT_CASE(32)
+        FC_FFT_TILES(FC_FFT_CASE)
 #undef FC_FFT_CASE
     }
     *handled = false;
@@ -1143,25 +914,23 @@ cudaError_t fc_launch_kernel_transform_fast(const Geometry &g, const ConvConsts 
                                             float *Vlo, int split, cudaStream_t s, int *handled) {
     *handled = 1;
     if (g.method == CONV_WINOGRAD) {
-        if (g.t == 4 && g.r == 3) return launch_nk1_wino<4, 3>(g, hc, w, V, Vlo, split, s);
-        if (g.t == 6 && g.r == 3) return launch_nk1_wino<6, 3>(g, hc, w, V, Vlo, split, s);
-        if (g.t == 8 && g.r == 3) return launch_nk1_wino<8, 3>(g, hc, w, V, Vlo, split, s);
-        if (g.t == 6 && g.r == 5) return launch_nk1_wino<6, 5>(g, hc, w, V, Vlo, split, s);
-    } else if (g.r == 3) {
+#define FC_NK1W_CASE(TT, MM) \
+    if (g.t == TT && g.m == MM) return launch_nk1_wino<TT, TT - MM + 1>(g, hc, w, V, Vlo, split, s);
+        FC_WINO_TILES(FC_NK1W_CASE)
+#undef FC_NK1W_CASE
+    } else if (g.r == 3) {  // every FFT tile edge with NK2 / NK4 codelets (FC_FFT_TILES)
         switch (g.t) {
-            case 8: return launch_nk1_fft<8, 3>(g, w, V, Vlo, split, s);
-            case 9: return launch_nk1_fft<9, 3>(g, w, V, Vlo, split, s);
-            case 10: return launch_nk1_fft<10, 3>(g, w, V, Vlo, split, s);
-            case 16: return launch_nk1_fft<16, 3>(g, w, V, Vlo, split, s);
-            case 24: return launch_nk1_fft<24, 3>(g, w, V, Vlo, split, s);
-            case 27: return launch_nk1_fft<27, 3>(g, w, V, Vlo, split, s);
-            case 32: return launch_nk1_fft<32, 3>(g, w, V, Vlo, split, s);
+#define FC_NK1_CASE(TT) \
+    case TT: return launch_nk1_fft<TT, 3>(g, w, V, Vlo, split, s);
+            FC_FFT_TILES(FC_NK1_CASE)
+#undef FC_NK1_CASE
         }
     } else if (g.r == 5) {
         switch (g.t) {
-            case 13: return launch_nk1_fft<13, 5>(g, w, V, Vlo, split, s);
-            case 18: return launch_nk1_fft<18, 5>(g, w, V, Vlo, split, s);
-            case 31: return launch_nk1_fft<31, 5>(g, w, V, Vlo, split, s);
+#define FC_NK1_CASE(TT) \
+    case TT: if (TT >= 5) return launch_nk1_fft<(TT >= 5 ? TT : 5), 5>(g, w, V, Vlo, split, s); break;
+            FC_FFT_TILES(FC_NK1_CASE)
+#undef FC_NK1_CASE
         }
     }
     *handled = 0;
@@ -1174,4 +943,24 @@ cudaError_t fc_launch_transform_fast(const Geometry &g, const ConvConsts &hc, co
     cudaError_t e = dispatch(g, hc, src, dst, forward != 0, s, &h);
     *handled = h ? 1 : 0;
     return e;
+}
+
+int fc_fast_transforms(int method, int t, int m, int r) {
+    if (method == CONV_WINOGRAD) {
+#define FC_WINO_HAVE(TT, MM) \
+    if (t == TT && m == MM) return 1;
+        FC_WINO_TILES(FC_WINO_HAVE)
+#undef FC_WINO_HAVE
+        return 0;
+    }
+    if (method != CONV_REGULAR_FFT && method != CONV_GAUSS_FFT) return 0;
+    (void)m;
+    (void)r;
+    switch (t) {
+#define FC_FFT_HAVE(TT) \
+    case TT: return 1;
+        FC_FFT_TILES(FC_FFT_HAVE)
+#undef FC_FFT_HAVE
+    }
+    return 0;
 }

@@ -59,6 +59,26 @@ def max_over_ranks(x: float, device=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(x: float, device=None) -> float:
+    """Sum of a scalar over ranks (whole-job byte counts)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def all_gather_scalar(x: float, device=None) -> list:
+    """[x of rank 0, x of rank 1, ...] (per-rank timings for the bench line)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return [float(x)]
+    world = dist.get_world_size()
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    bufs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(bufs, t)
+    return [float(b.item()) for b in bufs]
+
+
 def gather_batch(local: torch.Tensor, B: int, world: int) -> torch.Tensor:
     """All-gather per-rank output shards [b_lo:b_hi] into the full [B, ...] tensor
     (untimed; parity only).  Shards may differ in size by one image."""

@@ -38,7 +38,7 @@ def test_status_strings(lib):
 @pytest.mark.parametrize("args,status", [
     ((0, 4, 4, 16, 16, 3, "winograd", 2), 1),
     ((1, 4, 4, 2, 16, 3, "winograd", 2), 1),      # H < r
-    ((1, 4, 4, 16, 16, 3, "regular_fft", 0), 1),  # m < 1
+    ((1, 4, 4, 16, 16, 3, "regular_fft", -1), 1),  # m < 0 (m = 0: the planner picks)
     ((1, 4, 4, 16, 16, 3, "winograd", 7), 2),     # t = 9 > 8
     ((1, 4, 4, 16, 16, 1, "winograd", 4), 2),     # r < 2
     ((1, 4, 4, 99, 99, 3, "regular_fft", 63), 2),  # t = 65 > 64
@@ -105,7 +105,7 @@ def test_algorithmic_costs_vgg32(lib):
     assert g14["alg_bytes"][2] == pytest.approx(4 * 3 * th * (B * 16 * C + C * Co + B * 16 * Co))
 
 
-def test_gauss_epilogue_combine_choice(lib, monkeypatch):
+def test_gauss_epilogue_combine_choice(lib):
     """where the plan combines Gauss in the contraction's epilogue (X at w = 2)
     NK4 moves what Regular-FFT's does and NK3 writes 2/3 of the three-plane X."""
     B, C, Co, x, r, th = 64, 64, 64, 226, 3, 16 * 9  # VGG-1.2, m = 14: HBM-bound, combined
@@ -115,11 +115,12 @@ def test_gauss_epilogue_combine_choice(lib, monkeypatch):
     assert g["x_planes"] == 2 and g["bytes_X"] == 2 * th * Co * g["BN_pad"] * 4
     assert g["alg_bytes"][3] == pytest.approx(f["alg_bytes"][3])
     assert g["alg_bytes"][2] == pytest.approx(4 * 3 * th * (BN * C + C * Co) + 4 * 2 * th * BN * Co)
-    monkeypatch.setenv("FASTCONV_GC", "0")
-    g3 = fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14)
+    g3 = fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14, gauss_combine=0)
     assert g3["x_planes"] == 3 and g3["bytes_X"] == 3 * th * Co * g3["BN_pad"] * 4
-    monkeypatch.setenv("FASTCONV_GC", "1")
-    assert fc.plan_query(64, 256, 256, 58, 58, 3, "gauss_fft", 14)["x_planes"] == 2
+    assert fc.plan_query(64, 256, 256, 58, 58, 3, "gauss_fft", 14, gauss_combine=1)["x_planes"] == 2
+    # the combine needs the F16X3 contraction: 3xTF32 / FFMA plans keep three planes
+    assert fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14, gemm="tcgen05")["x_planes"] == 3
+    assert fc.plan_query(B, C, Co, x, x, r, "gauss_fft", 14, gemm="ffma", gauss_combine=1)["x_planes"] == 3
     # C' % 32 != 0: never combined
     g_odd = fc.plan_query(2, 8, 40, 20, 20, 3, "gauss_fft", 6)
     assert g_odd["x_planes"] == 3 and g_odd["bytes_X"] == 3 * g_odd["E"] * 40 * g_odd["BN_pad"] * 4
@@ -179,3 +180,54 @@ def test_plan_without_gpu_fails_cleanly(lib):
     h = ctypes.c_void_p()
     st = lib.conv_plan_ex(ctypes.byref(h), 1, 4, 4, 16, 16, 3, 1, 2, 0)
     assert st == 4 and not h.value  # CONV_ERR_CUDA, no plan returned
+
+
+def test_library_reads_no_environment():
+    """Every plan choice comes from the arguments and conv_plan_options (no getenv in csrc/)."""
+    import glob
+    import os
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1809_07851_b200", "csrc")
+    for f in glob.glob(os.path.join(root, "*")):
+        assert "getenv" not in open(f).read(), f
+
+
+def test_plan_options_validation(lib):
+    o = fc.options()
+    assert (o.gemm, o.gauss_combine, o.complex_mode, o.chunk_images, o.generic_transforms, o.single_cta_mma,
+            o.e2e_chunks) == (0, -1, -1, 0, 0, 0, 0)
+    info = fc.PlanInfo()
+    bad = fc.options(gauss_combine=2)
+    assert lib.conv_plan_query_opts(1, 4, 4, 16, 16, 3, 1, 4, ctypes.byref(bad), ctypes.byref(info)) == 1
+    bad = fc.options()
+    bad.struct_size = 4
+    assert lib.conv_plan_query_opts(1, 4, 4, 16, 16, 3, 1, 4, ctypes.byref(bad), ctypes.byref(info)) == 1
+    # NULL options = defaults
+    assert lib.conv_plan_query_opts(1, 4, 4, 16, 16, 3, 1, 4, None, ctypes.byref(info)) == 0
+    # complex mode off: the Regular-FFT V holds the real embedding (4x the (V_r, V_i) planes' entries)
+    on = fc.plan_query(64, 256, 256, 58, 58, 3, "regular_fft", 14)
+    off = fc.plan_query(64, 256, 256, 58, 58, 3, "regular_fft", 14, complex_mode=0)
+    assert off["bytes_V"] > on["bytes_V"]
+    # batch chunks
+    ch = fc.plan_query(64, 256, 256, 58, 58, 3, "winograd", 4, chunk_images=8)
+    assert (ch["chunk"], ch["nchunks"]) == (8, 8)
+
+
+def test_best_m_model(lib):
+    """conv_plan_best_m: the paper's stage-sum model over every compiled tile,
+    the argmin returned; m = 0 in conv_plan_query resolves to it."""
+    for method in ("winograd", "regular_fft", "gauss_fft"):
+        m, ms, cand = fc.best_m(64, 256, 256, 58, 58, 3, method)
+        assert m in cand and ms == pytest.approx(min(cand.values()))
+        assert all(cand[k] > ms or k >= m for k in cand)  # ties keep the smaller m
+        assert fc.plan_query(64, 256, 256, 58, 58, 3, method, 0)["m"] == m
+    # Winograd candidates: the compiled (t, m) pairs with t <= 8 for r = 3
+    _, _, cw = fc.best_m(64, 256, 256, 58, 58, 3, "winograd")
+    assert sorted(cw) == [2, 3, 4, 6]
+    # FFT candidates: every codelet t <= 32
+    _, _, cf = fc.best_m(64, 64, 64, 226, 226, 3, "regular_fft")
+    assert sorted(k + 2 for k in cf) == [4, 5, 6, 7, 8, 9, 10, 12, 13, 14, 15, 16, 18, 20, 21, 24, 25, 27, 28, 30,
+                                         31, 32]
+    with pytest.raises(fc.ConvError):
+        fc.best_m(1, 4, 4, 16, 16, 3, "direct")
+    with pytest.raises(fc.ConvError):
+        fc.plan_query(1, 4, 4, 16, 16, 3, "winograd", -1)

@@ -27,6 +27,33 @@ def test_reference_arm_json_line():
 import pytest  # noqa: E402
 
 
+def test_reference_arm_under_torchrun_world2():
+    """N > 1 launch of the reference arm (torchrun, gloo): rank 0 alone prints one line with
+    n_gpus 2, the other rank exits 0 without work."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl",
+                          "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--reference-budget-s", "3"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_gpus_mismatch_is_an_error():
+    """Under a torchrun environment, --gpus must equal WORLD_SIZE."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1"], cwd=ROOT, capture_output=True,
+                         text=True, timeout=300, env=env)
+    assert res.returncode == 2 and "WORLD_SIZE" in res.stderr
+
+
 @pytest.mark.gpu
 def test_fastconv_arm_json_line():
     """The GPU arm of bench.py (short run) prints one JSON line with the contract's keys and

@@ -45,15 +45,14 @@ RUNS = [("winograd", 2), ("winograd", 4), ("winograd", 6), ("regular_fft", 6), (
         ("gauss_fft", 6), ("gauss_fft", 14), ("direct", 0)]
 
 
-VARIANTS = [("auto", None), ("tcgen05", None), ("ffma", None), ("auto", "FASTCONV_GENERIC_TRANSFORMS"),
-            ("auto", "FASTCONV_PLANE"), ("auto", "FASTCONV_CHUNK")]
+VARIANTS = [("auto", None), ("tcgen05", None), ("ffma", None), ("auto", "generic_transforms"),
+            ("auto", "chunk_images"), ("auto", "single_cta_mma")]
 
 
-@pytest.mark.parametrize("gemm,env", VARIANTS)
+@pytest.mark.parametrize("gemm,opt", VARIANTS)
 @pytest.mark.parametrize("shape", CASES)
-def test_no_out_of_bounds_access(shape, gemm, env, monkeypatch):
-    if env:  # runtime-t transforms / TMA plane pipeline / one-image L2 chunks
-        monkeypatch.setenv(env, "1")
+def test_no_out_of_bounds_access(shape, gemm, opt):
+    opts = {opt: 1} if opt else {}  # runtime-t transforms / one-image chunks / single-CTA MMA tiles
     cfg = synth.custom(*shape, seed=97, dist="normal")
     I, W = synth.make_inputs(cfg)
     O = oracle.conv_fp64(I, W)
@@ -62,7 +61,8 @@ def test_no_out_of_bounds_access(shape, gemm, env, monkeypatch):
             continue
         if method == "direct" and gemm != "auto":
             continue
-        p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm if method != "direct" else "auto")
+        p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm if method != "direct" else "auto",
+                    **opts)
         xb, x = _guarded(I.numel(), float("nan"))
         wb, w = _guarded(W.numel(), float("nan"))
         x.copy_(I.reshape(-1))

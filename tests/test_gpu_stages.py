@@ -73,12 +73,14 @@ def test_stages(fc, method, m, gemm, shape):
     # U is blocked by 128 tiles: [BN_pad / 128][Z][K][128] (fc_u_off) -> [Z][K][BN]
     U = (_ws_view(ws, p.layout["U"], Z * K * BNp).reshape(BNp // 128, Z, K, 128).permute(1, 2, 0, 3)
          .reshape(Z, K, BNp)[:, :, :BN].double().cpu().numpy())
-    if gemm == "f16x3":  # NK2's reduction: exactly max|U| (Winograd), a bound |re|+|im| (FFT)
-        umax = ws[p.layout["umax"]:p.layout["umax"] + 4].view(torch.float32).item()
-        if method == "winograd":
-            assert umax == np.abs(U).max()
-        else:
-            assert np.abs(U).max() <= umax <= 2.0 * np.abs(U).max()
+    if gemm == "f16x3":  # NK2's per-image reduction: exactly max|U_b| (Winograd), a bound |re|+|im| (FFT)
+        umax = ws[p.layout["umax"]:p.layout["umax"] + 4 * cfg.B].view(torch.float32).double().cpu().numpy()
+        for b in range(cfg.B):
+            ub = np.abs(U[:, :, b * N:(b + 1) * N]).max()
+            if method == "winograd":
+                assert umax[b] == ub, b
+            else:
+                assert ub <= umax[b] <= 2.0 * ub, b
     In = I.double().numpy()
     Wn = W.double().numpy()
     tiles = _tiles(In, m, cfg.r, info["n_h"], info["n_w"])  # [B][C][N][t][t]
