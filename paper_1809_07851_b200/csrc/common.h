@@ -272,6 +272,15 @@ cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w,
                              cudaStream_t s);
 int fc_tcgen05_available();
 cudaError_t fc_init_twiddles();
+// FFT NK2 (forward) / NK4 transforms with compile-time t, split over fft_xforms_{a,b,c}.cu;
+// *handled = 0 when that unit has no codelet for g.t
+cudaError_t fc_fft_xform_a(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
+cudaError_t fc_fft_xform_b(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
+cudaError_t fc_fft_xform_c(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
+cudaError_t fc_fft_twiddles_a();
+cudaError_t fc_fft_twiddles_b();
+cudaError_t fc_fft_twiddles_c();
+
 // compile-time-t transforms; *handled = 0 when t has no specialisation
 cudaError_t fc_launch_kernel_transform_fast(const Geometry &g, const ConvConsts &hc, const float *w, float *V,
                                             float *Vlo, int split, cudaStream_t s, int *handled);

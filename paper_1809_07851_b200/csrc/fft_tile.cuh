@@ -11,6 +11,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
+#include <mutex>
+
 namespace fct {
 
 struct cf {
@@ -129,7 +132,29 @@ __device__ __forceinline__ void fft(cf *x) {
     }
 }
 
+// Host: upload THIS translation unit's copy of c_tw (without -rdc every TU that includes
+// this header has its own __constant__ table) to the current device, once per device
+// (thread-safe).  Called at plan creation (fc_init_twiddles), never inside a capture.
+static inline cudaError_t upload_twiddles() {
+    static std::mutex mu;
+    static unsigned long long done_mask = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev < 64 && ((done_mask >> dev) & 1ull)) return cudaSuccess;
+    static float2 tab[kTwiddleCount];
+    for (int N = 1; N <= 64; ++N)
+        for (int k = 0; k < N; ++k) {  // fp64, rounded once (reading R11)
+            const double ang = 2.0 * 3.14159265358979323846 * (double)k / (double)N;
+            tab[tw_base(N) + k] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        }
+    e = cudaMemcpyToSymbol(c_tw, tab, sizeof(tab));
+    if (e == cudaSuccess && dev < 64) done_mask |= 1ull << dev;
+    return e;
+}
+
 }  // namespace fct
 
-// host: upload the twiddle table to the current device once (thread-safe)
+// host: upload every transform translation unit's twiddle table to the current device
 cudaError_t fc_init_twiddles();

@@ -397,3 +397,25 @@ def test_cuda_graph_errors():
     assert lib.conv_graph_create(p._h, None, None, None, None, 0, 1, 0, ctypes.byref(h)) == 1
     assert lib.conv_graph_launch(None, None) == 1
     lib.conv_graph_destroy(None)
+
+
+@pytest.mark.parametrize("method", ["regular_fft", "gauss_fft"])
+@pytest.mark.parametrize("shape", [(3, 16, 64, 37, 33, 3), (2, 12, 32, 35, 29, 5)])
+def test_every_fft_codelet(method, shape):
+    """Every compiled FFT tile edge t <= 32 (the three codelet translation units, the tiles the
+    planner's sweep and conv_plan_best_m choose from) meets the oracle bar, Regular and Gauss
+    (three planes and combined in the contraction's epilogue)."""
+    cfg = synth.custom(*shape, seed=121, dist="normal")
+    I, W = synth.make_inputs(cfg)
+    O = oracle.conv_fp64(I, W)
+    x, w = I.cuda(), W.cuda()
+    for t in [4, 5, 6, 7, 8, 9, 10, 12, 13, 14, 15, 16, 18, 20, 21, 24, 25, 27, 28, 30, 31, 32]:
+        m = t - cfg.r + 1
+        if m < 1:
+            continue
+        for gcomb in ((-1,) if method == "regular_fft" else (0, 1)):
+            kw = {} if gcomb < 0 else {"gauss_combine": gcomb}
+            p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, **kw)
+            y = p.forward(x, w)
+            torch.cuda.synchronize()
+            assert rel_err(y.cpu().double().numpy(), O) <= 1e-5, (t, gcomb)
