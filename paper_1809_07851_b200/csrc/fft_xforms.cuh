@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     const int ntiles = nimg * ntr * g.n_w;
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
     extern __shared__ float2 zs[];                                     // [ntiles][S]
-    float *so = reinterpret_cast<float *>(zs + (size_t)IPC * R * g.n_w * S);  // [nimg*ntr*m][SWo]
+    float *so = reinterpret_cast<float *>(zs + (((size_t)IPC * R * g.n_w * S + 1) & ~(size_t)1));  // [nimg*ntr*m][SWo]
     const size_t estride = (size_t)g.Xm * g.BN_pad;
     // (stepping these loads by an opaque byte stride, as nk4_wino does, measured slower here:
     // VGG-1.2 t = 27 / 32 NK4 +7-9%, three-plane Gauss +13%)
@@ -254,9 +254,11 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
         // whole images when they fit (IPC images), else strips of R tile rows
         const int Sm = (g.m * H) % 2 ? g.m * H : g.m * H + 1;
-        const int SWo = g.n_w * g.m;
+        // staged output pitch: n_w m rounded up to 16 bytes when the output rows are (vector copy-out)
+        const int SWo = (g.Wo & 3) == 0 ? (g.n_w * g.m + 3) & ~3 : g.n_w * g.m;
         auto smem_of = [&](int ipc, int r) {
-            return (size_t)ipc * r * g.n_w * Sm * sizeof(float2) + (size_t)ipc * r * g.m * SWo * sizeof(float);
+            return (((size_t)ipc * r * g.n_w * Sm + 1) & ~(size_t)1) * sizeof(float2) +
+                   (size_t)ipc * r * g.m * SWo * sizeof(float);
         };
         constexpr int items_env = 256;
         // at least 32 tiles per CTA: each (l, c') run of X a warp loads is then >= 128 bytes

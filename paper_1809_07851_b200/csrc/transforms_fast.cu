@@ -506,7 +506,7 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
         }
     } else {
         // about 256 tiles per CTA: strips of one image, or several whole images
-        const int SWo = g.n_w * g.m;
+        const int SWo = (g.Wo & 3) == 0 ? (g.n_w * g.m + 3) & ~3 : g.n_w * g.m;  // 16-byte staged rows
         constexpr int target = 256;
         int R = wino_strip_rows(g, SWo), IPC = 1;
         if (R * g.n_w > target) R = target / g.n_w > 0 ? target / g.n_w : 1;
