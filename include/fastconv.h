@@ -136,6 +136,12 @@ typedef struct {
     int nchunks;        /* ceil(B / chunk) */
     int gemm;           /* the contraction implementation the plan runs (conv_gemm_impl;
                            CONV_GEMM_AUTO resolved; conv_plan_query reports AUTO's default) */
+    /* N-dimensional plans (conv_plan_nd): nd = 1..3 and the per-axis sizes right-aligned in
+     * 3 slots (slot 2 = the last, fastest axis; unused leading slots hold 1).  2-D plans report
+     * nd = 2 with slots 1, 2 = (H, W); H, W, r, m, t, n_h, n_w above then describe the last
+     * two axes. */
+    int nd;
+    int in_shape[3], kernel_shape[3], m_shape[3], t_shape[3], tiles[3], out_shape[3];
     int x_planes;       /* real planes of X per transformed element: 1 Winograd, 2 Regular-FFT,
                            3 Gauss-FFT (T1, T2, T3), or 2 when the F16X3 contraction combines
                            Gauss in its epilogue (Re = T1 - T3, Im = T1 + T2; C' % 32 == 0;
@@ -181,6 +187,25 @@ conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W,
                          conv_method method, int m, conv_gemm_impl gemm);
 conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
                            conv_method method, int m, const conv_plan_options *opts);
+
+/* N-dimensional and non-isotropic layers ("support an arbitrary
+ * number of dimensions, as well as non-isotropic kernels"): nd = 1, 2 or 3 spatial axes,
+ *   in  [B][C][in_shape[0]]...[in_shape[nd-1]],   w [C'][C][kernel_shape[0]]...,
+ *   out [B][C'][in_shape[d] - kernel_shape[d] + 1 ...]      (valid cross-correlation),
+ * with output tile m[d] per axis (t_d = m[d] + kernel_shape[d] - 1; Winograd F(m_d, r_d)
+ * per axis with t_d <= 8, r_d = 1 axes are identities; FFT t_d <= 64 with the half
+ * spectrum on the last axis).  The transforms are the generic separable kernels of
+ * transforms_nd.cu; the contraction is the same tcgen05 / FFMA NK3.  nd = 2 with a square
+ * kernel and equal tiles is the 2-D plan (the compile-time codelets).  m is ignored for
+ * CONV_DIRECT (may be NULL).  All other entry points (conv_forward, _cached, _host, graphs,
+ * timers) accept these plans.  Errors as conv_plan, plus INVALID_ARG for nd outside 1..3 or
+ * NULL shape arrays, UNSUPPORTED for tiles whose t-volume exceeds 12800 elements. */
+conv_status conv_plan_nd(conv_plan_t *out, int nd, int B, int C, int Cout, const int *in_shape,
+                         const int *kernel_shape, conv_method method, const int *m,
+                         const conv_plan_options *opts);
+conv_status conv_plan_query_nd(int nd, int B, int C, int Cout, const int *in_shape, const int *kernel_shape,
+                               conv_method method, const int *m, const conv_plan_options *opts,
+                               conv_plan_info *info);
 
 conv_status conv_plan_get_info(conv_plan_t p, conv_plan_info *info);
 

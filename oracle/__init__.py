@@ -46,6 +46,9 @@ def _load():
         lib.oracle_conv_fp64.restype = ctypes.c_int
         lib.oracle_conv_fp64_sampled.argtypes = [f32p, f32p, i64p, ctypes.c_longlong, f64p] + [ctypes.c_int] * 6
         lib.oracle_conv_fp64_sampled.restype = ctypes.c_int
+        ip = ctypes.POINTER(ctypes.c_int)
+        lib.oracle_conv_nd_fp64.argtypes = [f32p, f32p, f64p] + [ctypes.c_int] * 4 + [ip, ip]
+        lib.oracle_conv_nd_fp64.restype = ctypes.c_int
         lib.oracle_num_threads.argtypes = []
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -103,6 +106,29 @@ def conv_fp64_sampled(I, W, idx) -> np.ndarray:
     if rc != 0:
         raise ValueError("oracle_conv_fp64_sampled rejected the shape or an index")
     return out
+
+
+def conv_nd_fp64(I, W) -> np.ndarray:
+    """N-dimensional, non-isotropic valid cross-correlation in fp64 (P:926-929 extension of
+    Eq. 5): I [B][C][n_0..], W [C'][C][r_0..] float32 with 1..3 spatial axes; returns float64
+    [B][C'][n_0 - r_0 + 1 ..]."""
+    I = _as_f32(I)
+    W = _as_f32(W)
+    nd = I.ndim - 2
+    if nd < 1 or nd > 3 or W.ndim != I.ndim or W.shape[1] != I.shape[1]:
+        raise ValueError("shape mismatch between input and weights")
+    B, C = I.shape[:2]
+    Co = W.shape[0]
+    ins, ks = list(I.shape[2:]), list(W.shape[2:])
+    O = np.empty((B, Co) + tuple(a - k + 1 for a, k in zip(ins, ks)), dtype=np.float64)
+    ia = (ctypes.c_int * 3)(*ins)
+    ka = (ctypes.c_int * 3)(*ks)
+    rc = _load().oracle_conv_nd_fp64(
+        I.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), W.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+        O.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), nd, B, C, Co, ia, ka)
+    if rc != 0:
+        raise ValueError("oracle_conv_nd_fp64 rejected the shape")
+    return O
 
 
 def num_threads() -> int:

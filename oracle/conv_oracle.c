@@ -100,6 +100,53 @@ int oracle_conv_fp64_sampled(const float *I, const float *Wt,
     return 0;
 }
 
+/* N-dimensional, non-isotropic form of the same definition (PAPER.md P:926-929:
+ * "Extension to non-isotropic and N-dimensional images and kernels ... is straightforward"):
+ *
+ *     O[b][c'][o_0]..[o_{nd-1}] = sum_{c<C} sum_{p_0<r_0} .. sum_{p_{nd-1}<r_{nd-1}}
+ *                                 (double)I[b][c][o_0+p_0]..[o_{nd-1}+p_{nd-1}]
+ *                                 * (double)W[c'][c][p_0]..[p_{nd-1}]
+ *
+ * for 0 <= o_d < in[d] - r[d] + 1, nd = 1..3, row-major tensors.  Each output is summed
+ * sequentially in (c, p_0, .., p_{nd-1}) order; parallel over (b, c') only.
+ * Returns 0, or -1 on an invalid shape. */
+int oracle_conv_nd_fp64(const float *I, const float *Wt, double *O, int nd, int B, int C, int Cout,
+                        const int *in, const int *r)
+{
+    if (nd < 1 || nd > 3 || B < 1 || C < 1 || Cout < 1) return -1;
+    int n[3] = {1, 1, 1}, k[3] = {1, 1, 1}, o[3] = {1, 1, 1};
+    for (int d = 0; d < nd; ++d) {
+        if (in[d] < 1 || r[d] < 1 || in[d] < r[d]) return -1;
+        n[3 - nd + d] = in[d];
+        k[3 - nd + d] = r[d];
+        o[3 - nd + d] = in[d] - r[d] + 1;
+    }
+    const size_t vin = (size_t)n[0] * n[1] * n[2], vout = (size_t)o[0] * o[1] * o[2];
+    const size_t kv = (size_t)k[0] * k[1] * k[2];
+    const long long planes = (long long)B * Cout;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long bc = 0; bc < planes; ++bc) {
+        const int b = (int)(bc / Cout), co = (int)(bc % Cout);
+        double *out = O + (size_t)bc * vout;
+        for (int i0 = 0; i0 < o[0]; ++i0)
+            for (int i1 = 0; i1 < o[1]; ++i1)
+                for (int i2 = 0; i2 < o[2]; ++i2) {
+                    double acc = 0.0;
+                    for (int c = 0; c < C; ++c) {
+                        const float *img = I + ((size_t)b * C + c) * vin;
+                        const float *ker = Wt + ((size_t)co * C + c) * kv;
+                        for (int p0 = 0; p0 < k[0]; ++p0)
+                            for (int p1 = 0; p1 < k[1]; ++p1)
+                                for (int p2 = 0; p2 < k[2]; ++p2)
+                                    acc += (double)img[((size_t)(i0 + p0) * n[1] + (i1 + p1)) * n[2] + (i2 + p2)] *
+                                           (double)ker[((size_t)p0 * k[1] + p1) * k[2] + p2];
+                    }
+                    out[((size_t)i0 * o[1] + i1) * o[2] + i2] = acc;
+                }
+    }
+    return 0;
+}
+
 /* Threads the OpenMP runtime will use (reported as cpu_baseline.cores). */
 int oracle_num_threads(void)
 {

@@ -65,13 +65,16 @@ class PlanInfo(ctypes.Structure):
                 [(n, ctypes.c_size_t) for n in ("bytes_U", "bytes_V", "bytes_X", "workspace_bytes")] +
                 [("alg_bytes", ctypes.c_double * 4), ("alg_flops", ctypes.c_double * 4),
                  ("direct_flops", ctypes.c_double), ("chunk", ctypes.c_int), ("nchunks", ctypes.c_int),
-                 ("gemm", ctypes.c_int), ("x_planes", ctypes.c_int)])
+                 ("gemm", ctypes.c_int), ("nd", ctypes.c_int)] +
+                [(n, ctypes.c_int * 3) for n in ("in_shape", "kernel_shape", "m_shape", "t_shape", "tiles",
+                                                 "out_shape")] +
+                [("x_planes", ctypes.c_int)])
 
     def as_dict(self) -> dict:
         d = {}
         for name, _ in self._fields_:
             v = getattr(self, name)
-            d[name] = list(v) if name.startswith("alg_") else v
+            d[name] = list(v) if isinstance(v, ctypes.Array) else v
         return d
 
 
@@ -105,6 +108,10 @@ def load(build_if_missing: bool = False):
         "conv_plan": ([ctypes.POINTER(vp)] + [i] * 8, i),
         "conv_plan_ex": ([ctypes.POINTER(vp)] + [i] * 9, i),
         "conv_plan_opts": ([ctypes.POINTER(vp)] + [i] * 8 + [ctypes.POINTER(PlanOptions)], i),
+        "conv_plan_nd": ([ctypes.POINTER(vp)] + [i] * 4 + [ctypes.POINTER(i), ctypes.POINTER(i), i,
+                                                           ctypes.POINTER(i), ctypes.POINTER(PlanOptions)], i),
+        "conv_plan_query_nd": ([i] * 4 + [ctypes.POINTER(i), ctypes.POINTER(i), i, ctypes.POINTER(i),
+                                          ctypes.POINTER(PlanOptions), ctypes.POINTER(PlanInfo)], i),
         "conv_plan_get_info": ([vp, ctypes.POINTER(PlanInfo)], i),
         "conv_workspace_bytes": ([vp], sz),
         "conv_forward": ([vp, vp, vp, vp, vp, sz, vp], i),
@@ -156,6 +163,18 @@ def plan_query(B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto",
     info = PlanInfo()
     o = options(gemm, **opts)
     _check(load().conv_plan_query_opts(B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o), ctypes.byref(info)))
+    return info.as_dict()
+
+
+def plan_query_nd(B, C, Cout, in_shape, kernel_shape, method: str, m=None, gemm: str = "auto", **opts) -> dict:
+    """conv_plan_query_nd: geometry and algorithmic costs of an N-D / non-isotropic plan."""
+    nd = len(in_shape)
+    info = PlanInfo()
+    o = options(gemm, **opts)
+    ia = (ctypes.c_int * 3)(*in_shape)
+    ka = (ctypes.c_int * 3)(*kernel_shape)
+    ma = (ctypes.c_int * 3)(*(m or [1] * nd))
+    _check(load().conv_plan_query_nd(nd, B, C, Cout, ia, ka, METHODS[method], ma, ctypes.byref(o), ctypes.byref(info)))
     return info.as_dict()
 
 
@@ -212,11 +231,19 @@ def _check_tensor(x: torch.Tensor, name: str, shape=None):
 class Plan:
     """conv_plan(B, C, C', H, W, r, method, m) -- immutable; owns only host metadata + constants."""
 
-    def __init__(self, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto", **opts):
+    def __init__(self, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto", _nd=None, **opts):
         lib = load()
         h = ctypes.c_void_p()
         o = options(gemm, **opts)
-        _check(lib.conv_plan_opts(ctypes.byref(h), B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o)))
+        if _nd is None:
+            _check(lib.conv_plan_opts(ctypes.byref(h), B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o)))
+        else:
+            in_shape, k_shape, m_shape = _nd
+            nd = len(in_shape)
+            ia = (ctypes.c_int * 3)(*in_shape)
+            ka = (ctypes.c_int * 3)(*k_shape)
+            ma = (ctypes.c_int * 3)(*(m_shape or [1] * nd))
+            _check(lib.conv_plan_nd(ctypes.byref(h), nd, B, C, Cout, ia, ka, METHODS[method], ma, ctypes.byref(o)))
         self._h = h
         self.method = method
         info = PlanInfo()
@@ -231,9 +258,23 @@ class Plan:
         self.layout.update({"vscale": aux[0], "umax": aux[1]})
         self.gemm = gemm
         self.launches = int(lib.conv_forward_launch_count(h))
-        self.in_shape = (B, C, H, W)
-        self.w_shape = (Cout, C, r, r)
-        self.out_shape = (B, Cout, H - r + 1, W - r + 1)
+        if _nd is None:
+            self.in_shape = (B, C, H, W)
+            self.w_shape = (Cout, C, r, r)
+            self.out_shape = (B, Cout, H - r + 1, W - r + 1)
+        else:
+            self.in_shape = (B, C) + tuple(in_shape)
+            self.w_shape = (Cout, C) + tuple(k_shape)
+            self.out_shape = (B, Cout) + tuple(a - k + 1 for a, k in zip(in_shape, k_shape))
+
+    @classmethod
+    def nd(cls, B, C, Cout, in_shape, kernel_shape, method: str, m=None, gemm: str = "auto", **opts) -> "Plan":
+        """conv_plan_nd: 1-3 spatial axes, per-axis kernel sizes and output tiles m."""
+        in_shape, kernel_shape = tuple(in_shape), tuple(kernel_shape)
+        if len(in_shape) != len(kernel_shape) or not 1 <= len(in_shape) <= 3:
+            raise ValueError("in_shape and kernel_shape need the same length 1..3")
+        m = None if m is None else tuple(m)
+        return cls(B, C, Cout, 0, 0, 0, method, 0, gemm, _nd=(in_shape, kernel_shape, m), **opts)
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -218,7 +218,7 @@ static bool gauss_combine_pays(const Geometry &G, int force) {
     const double pad256 = std::ceil(BN / 256.0) * 256.0, pad128 = std::ceil(BN / 128.0) * 128.0;
     const double mma = 3.0 * 6.0 * E * C * Co;  // tensor FLOPs per padded column
     const double u = 4.0 * 3.0 * E * BN * C, x3 = 4.0 * 3.0 * E * BN * Co, x2 = x3 * 2.0 / 3.0;
-    const double o = 4.0 * G.B * Co * (double)G.Ho * G.Wo;
+    const double o = 4.0 * G.B * Co * (double)G.vout;
     // the 3-plane contraction also drops to 128-column tiles when 256 would pad B N by >= 25%
     const double r3 = 4.0 * pad256 >= 5.0 * pad128 ? mma * pad128 / r128 : mma * pad256 / r256;
     const double t3 = std::max(r3, (u + x3) / bw) + (x3 + o) / bw4;
@@ -334,13 +334,103 @@ conv_status fc_best_m(int B, int C, int Cout, int H, int W, int r, int method, c
     return CONV_OK;
 }
 
+// The part of the plan shared by 2-D and N-D layers: contraction shape (Z, M, K, Kp,
+// complex mode, Gauss combine) and the info block (workspace sizes, algorithmic bytes and
+// FLOPs of Table layer-stuff P:1025-1032 with c = C, c' = C', alpha = 1, generalised to
+// volumes: prod in_d, prod r_d, prod o_d).  G: B, C, Cout, method, t / E / N / BN(_pad),
+// planes, vin, vout, kvol, (nd axes) filled.
+static conv_status finish_geometry(Geometry &G, conv_plan_info *info, const conv_plan_options *opts) {
+    const conv_gemm_impl gemm = opts->gemm;
+    const int method = G.method, B = G.B, C = G.C, Cout = G.Cout;
+    if (method != CONV_DIRECT) {
+        G.divN = fc_fastdiv(G.N);
+        G.divNw = fc_fastdiv(G.n_w > 0 ? G.n_w : 1);
+        G.BN = (long long)B * G.N;
+        G.BN_pad = (G.BN + FC_TB - 1) / FC_TB * FC_TB;
+        if (G.BN >= (1LL << 31)) {
+            fc_set_error("too many tiles (B N = %lld)", G.BN);
+            return CONV_ERR_UNSUPPORTED;
+        }
+        if (method == CONV_REGULAR_FFT) {  // real embedding of the complex product
+            G.Z = G.E; G.M = 2 * Cout; G.K = 2 * C;
+        } else if (method == CONV_GAUSS_FFT) {
+            G.Z = 3 * G.E; G.M = Cout; G.K = C;
+        } else {
+            G.Z = G.E; G.M = Cout; G.K = C;
+        }
+        G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
+        const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
+        G.Kp = (G.K + kq - 1) / kq * kq;
+        G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G, opts->gauss_combine);
+        G.Xz = G.gc ? G.E : G.Z;
+        G.Xm = G.gc ? 2 * Cout : G.M;
+        G.cplx = 0;
+        if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % (G.vf16 ? 32 : 16) == 0 &&
+            opts->complex_mode != 0) {
+            G.cplx = 1;
+            G.Kp = (C + kq - 1) / kq * kq;
+        }
+    }
+    G.tc_1sm = opts->single_cta_mma;
+    if (!info) return CONV_OK;
+    conv_plan_info I;
+    memset(&I, 0, sizeof(I));
+    I.B = B; I.C = C; I.Cout = Cout; I.H = G.H; I.W = G.W; I.r = G.r; I.m = G.m; I.method = method;
+    I.Ho = G.Ho; I.Wo = G.Wo; I.t = G.t; I.n_h = G.n_h; I.n_w = G.n_w; I.N = G.N; I.h = G.h;
+    I.E = G.E; I.planes = G.planes; I.BN = G.BN; I.BN_pad = G.BN_pad;
+    I.gemm_Z = G.Z; I.gemm_M = G.M; I.gemm_K = G.K;
+    I.nd = G.nd ? G.nd : 2;
+    for (int d = 0; d < 3; ++d) {
+        I.in_shape[d] = G.ax_in[d]; I.kernel_shape[d] = G.ax_r[d]; I.m_shape[d] = G.ax_m[d];
+        I.t_shape[d] = G.ax_t[d]; I.tiles[d] = G.ax_n[d]; I.out_shape[d] = G.ax_o[d];
+    }
+    const double vin = (double)G.vin, vout = (double)G.vout, kv = (double)G.kvol;
+    I.direct_flops = 2.0 * B * (double)C * Cout * vout * kv;
+    I.chunk = B;
+    I.nchunks = 1;
+    I.gemm = gemm == CONV_GEMM_AUTO ? CONV_GEMM_TCGEN05_F16X3 : gemm;
+    I.x_planes = method == CONV_DIRECT ? 0 : (G.gc ? 2 : G.planes);
+    if (method != CONV_DIRECT) {
+        const int split = (gemm != CONV_GEMM_FFMA);
+        const size_t vb = fc_v_bytes(G);  // V_hi, then V_lo at the next 256 B boundary
+        I.bytes_V = split ? align256(vb) + vb : vb;
+        I.chunk = pick_chunk(G, opts->chunk_images);
+        if (G.vf16)  // + per-c' scales [2][C'] and the per-image max|U_b| words of a chunk
+            I.bytes_V = align256(I.bytes_V) + align256((size_t)2 * Cout * 4) + align256((size_t)I.chunk * 4);
+        I.nchunks = (B + I.chunk - 1) / I.chunk;
+        const Geometry Gc = fc_chunk_geometry(G, I.chunk);
+        I.BN_pad = Gc.BN_pad;
+        I.bytes_U = (size_t)G.Z * G.K * Gc.BN_pad * 4;
+        I.bytes_X = (size_t)G.Xz * G.Xm * Gc.BN_pad * 4;
+        I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
+        const double BCN = (double)B * C * G.N, BCpN = (double)B * Cout * G.N;
+        const double CCp = (double)C * Cout;
+        const double BN = (double)B * G.N;
+        // reals per transformed tile: wE = E (Winograd), 2E (Regular), 3E (Gauss)
+        const double wEr = method == CONV_GAUSS_FFT ? 3.0 * G.E : (method == CONV_REGULAR_FFT ? 2.0 * G.E : (double)G.E);
+        I.alg_bytes[0] = 4.0 * CCp * kv + 4.0 * wEr * CCp;
+        I.alg_bytes[1] = 4.0 * B * C * vin + 4.0 * wEr * BCN;
+        // X carries x_planes real planes per element (Gauss combined in NK3's epilogue: 2)
+        const double wX = G.gc ? 2.0 * G.E : wEr;
+        I.alg_bytes[2] = 4.0 * wEr * (BN * C + CCp) + 4.0 * wX * BN * Cout;
+        I.alg_bytes[3] = 4.0 * wX * BCpN + 4.0 * B * Cout * vout;
+        // element-wise FLOPs: 2t^2 BNCC' / 8 t h BNCC' / 6 t h BNCC'
+        const double k = method == CONV_WINOGRAD ? 2.0 : (method == CONV_REGULAR_FFT ? 8.0 : 6.0);
+        I.alg_flops[2] = k * G.E * BN * CCp;
+    } else {
+        I.alg_bytes[2] = 4.0 * B * C * vin + 4.0 * Cout * C * kv + 4.0 * B * Cout * vout;
+        I.alg_flops[2] = I.direct_flops;
+    }
+    *info = I;
+    return CONV_OK;
+}
+
 conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int method, int m,
                              Geometry *g, conv_plan_info *info, const conv_plan_options *opts) {
     {
         conv_status st = check_options(opts);
         if (st != CONV_OK) return st;
     }
-    const conv_gemm_impl gemm = opts->gemm;
     if (B < 1 || C < 1 || Cout < 1 || H < 1 || W < 1 || r < 1) {
         fc_set_error("sizes must be >= 1 (B=%d C=%d C'=%d H=%d W=%d r=%d)", B, C, Cout, H, W, r);
         return CONV_ERR_INVALID_ARG;
@@ -369,6 +459,14 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
     G.B = B; G.C = C; G.Cout = Cout; G.H = H; G.W = W; G.r = r; G.method = method;
     G.Ho = H - r + 1;
     G.Wo = W - r + 1;
+    G.nd = 0;
+    G.vin = (long long)H * W;
+    G.vout = (long long)G.Ho * G.Wo;
+    G.kvol = r * r;
+    G.ax_in[0] = 1; G.ax_in[1] = H; G.ax_in[2] = W;
+    G.ax_r[0] = 1; G.ax_r[1] = r; G.ax_r[2] = r;
+    G.ax_o[0] = 1; G.ax_o[1] = G.Ho; G.ax_o[2] = G.Wo;
+    G.ax_m[0] = G.ax_t[0] = G.ax_n[0] = G.ax_len[0] = 1;
     if (method == CONV_DIRECT) {
         G.m = 0;
     } else {
@@ -392,81 +490,116 @@ conv_status fc_fill_geometry(int B, int C, int Cout, int H, int W, int r, int me
         G.n_h = (G.Ho + m - 1) / m;
         G.n_w = (G.Wo + m - 1) / m;
         G.N = G.n_h * G.n_w;
-        G.divN = fc_fastdiv(G.N);
-        G.divNw = fc_fastdiv(G.n_w);
         G.E = G.t * G.h;
-        G.BN = (long long)B * G.N;
-        G.BN_pad = (G.BN + FC_TB - 1) / FC_TB * FC_TB;
-        if (method == CONV_REGULAR_FFT) {  // real embedding of the complex product
-            G.Z = G.E; G.M = 2 * Cout; G.K = 2 * C;
-        } else if (method == CONV_GAUSS_FFT) {
-            G.Z = 3 * G.E; G.M = Cout; G.K = C;
-        } else {
-            G.Z = G.E; G.M = Cout; G.K = C;
-        }
-        G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
-        const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
-        G.Kp = (G.K + kq - 1) / kq * kq;
-        G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G, opts->gauss_combine);
-        G.Xz = G.gc ? G.E : G.Z;
-        G.Xm = G.gc ? 2 * Cout : G.M;
-        G.cplx = 0;
-        if (method == CONV_REGULAR_FFT && gemm != CONV_GEMM_FFMA && Cout % 256 == 0 && C % (G.vf16 ? 32 : 16) == 0 &&
-            opts->complex_mode != 0) {
-            G.cplx = 1;
-            G.Kp = (C + kq - 1) / kq * kq;
-        }
+        G.ax_m[1] = G.ax_m[2] = m;
+        G.ax_t[1] = G.ax_t[2] = G.t;
+        G.ax_n[1] = G.n_h; G.ax_n[2] = G.n_w;
+        G.ax_len[1] = G.t; G.ax_len[2] = G.h;
     }
-    G.tc_1sm = opts->single_cta_mma;
+    conv_status st = finish_geometry(G, info, opts);
+    if (st != CONV_OK) return st;
     *g = G;
-    if (info) {
-        conv_plan_info I;
-        memset(&I, 0, sizeof(I));
-        I.B = B; I.C = C; I.Cout = Cout; I.H = H; I.W = W; I.r = r; I.m = G.m; I.method = method;
-        I.Ho = G.Ho; I.Wo = G.Wo; I.t = G.t; I.n_h = G.n_h; I.n_w = G.n_w; I.N = G.N; I.h = G.h;
-        I.E = G.E; I.planes = G.planes; I.BN = G.BN; I.BN_pad = G.BN_pad;
-        I.gemm_Z = G.Z; I.gemm_M = G.M; I.gemm_K = G.K;
-        I.direct_flops = 2.0 * B * (double)C * Cout * G.Ho * G.Wo * r * r;
-        I.chunk = B;
-        I.nchunks = 1;
-        I.gemm = gemm == CONV_GEMM_AUTO ? CONV_GEMM_TCGEN05_F16X3 : gemm;
-        I.x_planes = method == CONV_DIRECT ? 0 : (G.gc ? 2 : G.planes);
-        if (method != CONV_DIRECT) {
-            const int split = (gemm != CONV_GEMM_FFMA);
-            const size_t vb = fc_v_bytes(G);  // V_hi, then V_lo at the next 256 B boundary
-            I.bytes_V = split ? align256(vb) + vb : vb;
-            I.chunk = pick_chunk(G, opts->chunk_images);
-            if (G.vf16)  // + per-c' scales [2][C'] and the per-image max|U_b| words of a chunk
-                I.bytes_V = align256(I.bytes_V) + align256((size_t)2 * Cout * 4) + align256((size_t)I.chunk * 4);
-            I.nchunks = (B + I.chunk - 1) / I.chunk;
-            const Geometry Gc = fc_chunk_geometry(G, I.chunk);
-            I.BN_pad = Gc.BN_pad;
-            I.bytes_U = (size_t)G.Z * G.K * Gc.BN_pad * 4;
-            I.bytes_X = (size_t)G.Xz * G.Xm * Gc.BN_pad * 4;
-            I.workspace_bytes = align256(I.bytes_V) + align256(I.bytes_U) + align256(I.bytes_X);
-            // Table layer-stuff, c=C, c'=C', alpha=1; wE = reals per tile
-            const double wE = (double)G.planes * G.E * (method == CONV_WINOGRAD ? 1 : 1);
-            const double BCN = (double)B * C * G.N, BCpN = (double)B * Cout * G.N;
-            const double CCp = (double)C * Cout;
-            const double BN = (double)B * G.N;
-            const double wEr = method == CONV_GAUSS_FFT ? 3.0 * G.E : (method == CONV_REGULAR_FFT ? 2.0 * G.E : (double)G.E);
-            (void)wE;
-            I.alg_bytes[0] = 4.0 * CCp * r * r + 4.0 * wEr * CCp;
-            I.alg_bytes[1] = 4.0 * B * C * (double)H * W + 4.0 * wEr * BCN;
-            // X carries x_planes real planes per element (Gauss combined in NK3's epilogue: 2)
-            const double wX = G.gc ? 2.0 * G.E : wEr;
-            I.alg_bytes[2] = 4.0 * wEr * (BN * C + CCp) + 4.0 * wX * BN * Cout;
-            I.alg_bytes[3] = 4.0 * wX * BCpN + 4.0 * B * Cout * (double)G.Ho * G.Wo;
-            // element-wise FLOPs: 2t^2 BNCC' / 8 t h BNCC' / 6 t h BNCC'
-            const double k = method == CONV_WINOGRAD ? 2.0 : (method == CONV_REGULAR_FFT ? 8.0 : 6.0);
-            I.alg_flops[2] = k * G.E * BN * CCp;
-        } else {
-            I.alg_bytes[2] = 4.0 * B * C * (double)H * W + 4.0 * Cout * C * r * r +
-                             4.0 * B * Cout * (double)G.Ho * G.Wo;
-            I.alg_flops[2] = I.direct_flops;
-        }
-        *info = I;
+    return CONV_OK;
+}
+
+// N-dimensional / non-isotropic geometry (conv_plan_nd): per-axis sizes right-aligned in 3
+// slots.  nd == 2 with a square kernel and equal tiles is the 2-D isotropic plan (fast path).
+conv_status fc_fill_geometry_nd(int nd, int B, int C, int Cout, const int *in, const int *rk, int method,
+                                const int *mt, Geometry *g, conv_plan_info *info, const conv_plan_options *opts) {
+    conv_status st = check_options(opts);
+    if (st != CONV_OK) return st;
+    if (nd < 1 || nd > 3 || !in || !rk || (method != CONV_DIRECT && !mt)) {
+        fc_set_error("conv_plan_nd: nd must be 1..3 and the shape arrays non-NULL");
+        return CONV_ERR_INVALID_ARG;
     }
+    if (method < CONV_DIRECT || method > CONV_GAUSS_FFT) {
+        fc_set_error("unknown method %d", method);
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (nd == 2 && rk[0] == rk[1] && (method == CONV_DIRECT || (mt[0] == mt[1] && mt[0] > 0)))
+        return fc_fill_geometry(B, C, Cout, in[0], in[1], rk[0], method, method == CONV_DIRECT ? 0 : mt[0], g, info,
+                                opts);
+    if (B < 1 || C < 1 || Cout < 1) {
+        fc_set_error("sizes must be >= 1 (B=%d C=%d C'=%d)", B, C, Cout);
+        return CONV_ERR_INVALID_ARG;
+    }
+    Geometry G = {};
+    G.B = B; G.C = C; G.Cout = Cout; G.method = method; G.nd = nd;
+    G.vin = G.vout = 1;
+    G.kvol = 1;
+    long long ntile = 1, E = 1;
+    int tmax = 1;
+    for (int d = 0; d < 3; ++d) {
+        G.ax_in[d] = G.ax_r[d] = G.ax_m[d] = G.ax_t[d] = G.ax_n[d] = G.ax_o[d] = G.ax_len[d] = 1;
+    }
+    for (int i = 0; i < nd; ++i) {
+        const int d = 3 - nd + i;
+        if (in[i] < 1 || rk[i] < 1 || in[i] < rk[i]) {
+            fc_set_error("axis %d: input %d and kernel %d must be >= 1 with input >= kernel", i, in[i], rk[i]);
+            return CONV_ERR_INVALID_ARG;
+        }
+        G.ax_in[d] = in[i];
+        G.ax_r[d] = rk[i];
+        G.ax_o[d] = in[i] - rk[i] + 1;
+        G.vin *= in[i];
+        G.vout *= G.ax_o[d];
+        G.kvol *= rk[i];
+        if (method == CONV_DIRECT) continue;
+        if (mt[i] < 1) {
+            fc_set_error("axis %d: output tile m must be >= 1 (got %d)", i, mt[i]);
+            return CONV_ERR_INVALID_ARG;
+        }
+        G.ax_m[d] = mt[i];
+        G.ax_t[d] = mt[i] + rk[i] - 1;
+        if (method == CONV_WINOGRAD) {
+            if (rk[i] > 1 && (mt[i] < 2 || G.ax_t[d] > 8)) {
+                fc_set_error("axis %d: Winograd F(%d,%d) unsupported: need m>=2, t<=8 (r = 1 axes: any m)", i, mt[i],
+                             rk[i]);
+                return CONV_ERR_UNSUPPORTED;
+            }
+            if (rk[i] == 1 && mt[i] > 8) {
+                fc_set_error("axis %d: Winograd tile %d exceeds 8", i, mt[i]);
+                return CONV_ERR_UNSUPPORTED;
+            }
+        } else if (G.ax_t[d] > FC_MAX_T) {
+            fc_set_error("axis %d: FFT tile t=%d exceeds %d", i, G.ax_t[d], FC_MAX_T);
+            return CONV_ERR_UNSUPPORTED;
+        }
+        G.ax_n[d] = (G.ax_o[d] + mt[i] - 1) / mt[i];
+        G.ax_len[d] = (method != CONV_WINOGRAD && i == nd - 1) ? G.ax_t[d] / 2 + 1 : G.ax_t[d];
+        ntile *= G.ax_n[d];
+        E *= G.ax_len[d];
+        tmax = G.ax_t[d] > tmax ? G.ax_t[d] : tmax;
+    }
+    if ((long long)B * C * G.vin >= (1LL << 40) || (long long)Cout * C * G.kvol >= (1LL << 40) ||
+        (long long)B * Cout * G.vout >= (1LL << 40) || ntile >= (1LL << 31) || E >= (1LL << 20)) {
+        fc_set_error("tensor too large");
+        return CONV_ERR_UNSUPPORTED;
+    }
+    // 2-D-style fields for reporting (the last two axes)
+    G.H = G.ax_in[1]; G.W = G.ax_in[2]; G.Ho = G.ax_o[1]; G.Wo = G.ax_o[2];
+    G.r = G.ax_r[2];
+    if (method == CONV_DIRECT) {
+        G.m = 0;
+    } else {
+        G.m = G.ax_m[2];
+        G.t = G.ax_t[2];
+        G.h = G.ax_len[2];
+        G.n_h = G.ax_n[1];
+        G.n_w = G.ax_n[2];
+        G.N = (int)ntile;
+        G.E = (int)E;
+        G.planes = method == CONV_WINOGRAD ? 1 : (method == CONV_REGULAR_FFT ? 2 : 3);
+        const long long vt = (long long)G.ax_t[0] * G.ax_t[1] * G.ax_t[2];
+        if (vt * 16 > 200 * 1024) {
+            fc_set_error("N-D tile volume %lld too large for the generic transforms", vt);
+            return CONV_ERR_UNSUPPORTED;
+        }
+    }
+    (void)tmax;
+    st = finish_geometry(G, info, opts);
+    if (st != CONV_OK) return st;
+    *g = G;
     return CONV_OK;
 }
 
@@ -540,8 +673,10 @@ conv_status conv_winograd_matrices(int m, int r, double *AT, double *BT, double 
     return fc_winograd_rational(m, r, AT, BT, G);
 }
 
-conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
-                           conv_method method, int m, const conv_plan_options *opts_in) {
+// nd = 0: the 2-D isotropic plan (H, W, r, m); nd = 1..3: conv_plan_nd's shapes (in, rk, mt)
+static conv_status plan_create(conv_plan_t *out, int nd, int B, int C, int Cout, int H, int W, int r,
+                               conv_method method, int m, const int *in, const int *rk, const int *mt,
+                               const conv_plan_options *opts_in) {
     if (!out) {
         fc_set_error("NULL plan pointer");
         return CONV_ERR_INVALID_ARG;
@@ -564,13 +699,54 @@ conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int 
         return CONV_ERR_UNSUPPORTED;
     }
     opts.gemm = gemm;
-    conv_status st = fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &p->g, &p->info, &opts);
+    conv_status st = nd == 0 ? fc_fill_geometry(B, C, Cout, H, W, r, (int)method, m, &p->g, &p->info, &opts)
+                             : fc_fill_geometry_nd(nd, B, C, Cout, in, rk, (int)method, mt, &p->g, &p->info, &opts);
     if (st != CONV_OK) { free(p); return st; }
     p->gemm = gemm;
     const Geometry &g = p->g;
     ConvConsts &cc = p->host_consts;
     memset(&cc, 0, sizeof(cc));
-    if (method == CONV_WINOGRAD) {
+    NdConsts ndc;
+    memset(&ndc, 0, sizeof(ndc));
+    if (g.nd && method != CONV_DIRECT) {
+        // per-axis constants (exact rationals / fp64 twiddles, rounded once) and the F16X3 bound
+        // |V| <= prod_d (max_k sum_p |G_d[k][p]|) max|g|  (FFT: prod r_d / prod t_d, x2 Gauss)
+        double bound = method == CONV_GAUSS_FFT ? 2.0 : 1.0;
+        for (int d = 3 - g.nd; d < 3; ++d) {
+            const int md = g.ax_m[d], rd = g.ax_r[d], td = g.ax_t[d];
+            if (method == CONV_WINOGRAD) {
+                double at[64], bt[64], gm[64];
+                if (rd == 1) {  // F(m, 1): identity transforms, G = ones
+                    for (int i = 0; i < 64; ++i) at[i] = bt[i] = gm[i] = 0.0;
+                    for (int i = 0; i < td; ++i) {
+                        at[i * td + i] = bt[i * td + i] = 1.0;
+                        gm[i] = 1.0;
+                    }
+                } else {
+                    st = fc_winograd_rational(md, rd, at, bt, gm);
+                    if (st != CONV_OK) { free(p); return st; }
+                }
+                for (int i = 0; i < td * td; ++i) ndc.BT[d][i] = (float)bt[i];
+                for (int i = 0; i < td * rd; ++i) ndc.G[d][i] = (float)gm[i];
+                for (int i = 0; i < md * td; ++i) ndc.AT[d][i] = (float)at[i];
+                double rs = 0.0;
+                for (int k = 0; k < td; ++k) {
+                    double a_ = 0.0;
+                    for (int q = 0; q < rd; ++q) a_ += fabs(gm[k * rd + q]);
+                    rs = a_ > rs ? a_ : rs;
+                }
+                bound *= rs;
+            } else {
+                for (int j = 0; j < td; ++j) {
+                    const double ang = 2.0 * M_PI * (double)j / (double)td;
+                    ndc.cosv[d][j] = (float)cos(ang);
+                    ndc.sinv[d][j] = (float)sin(ang);
+                }
+                bound *= (double)rd / (double)td;
+            }
+        }
+        p->g.vbound = (float)bound;
+    } else if (method == CONV_WINOGRAD) {
         st = fc_winograd_rational(g.m, g.r, p->AT64, p->BT64, p->G64);
         if (st != CONV_OK) { free(p); return st; }
         for (int i = 0; i < g.t * g.t; ++i) cc.BT[i] = (float)p->BT64[i];
@@ -629,6 +805,17 @@ conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int 
             free(p);
             return CONV_ERR_CUDA;
         }
+        if (g.nd) {
+            e = cudaMalloc(&p->d_nd, sizeof(NdConsts));
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_nd, &ndc, sizeof(NdConsts), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) {
+                fc_set_error("N-D constants: %s", cudaGetErrorString(e));
+                if (p->d_nd) cudaFree(p->d_nd);
+                cudaFree(p->d_consts);
+                free(p);
+                return e == cudaErrorMemoryAllocation ? CONV_ERR_OUT_OF_MEMORY : CONV_ERR_CUDA;
+            }
+        }
         p->off_V = 0;
         const size_t vb = fc_v_bytes(g);
         p->off_Vlo = align256(vb);
@@ -657,6 +844,25 @@ conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int 
     return CONV_OK;
 }
 
+conv_status conv_plan_opts(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
+                           conv_method method, int m, const conv_plan_options *opts) {
+    return plan_create(out, 0, B, C, Cout, H, W, r, method, m, nullptr, nullptr, nullptr, opts);
+}
+
+conv_status conv_plan_nd(conv_plan_t *out, int nd, int B, int C, int Cout, const int *in_shape,
+                         const int *kernel_shape, conv_method method, const int *m, const conv_plan_options *opts) {
+    return plan_create(out, nd, B, C, Cout, 0, 0, 0, method, 0, in_shape, kernel_shape, m, opts);
+}
+
+conv_status conv_plan_query_nd(int nd, int B, int C, int Cout, const int *in_shape, const int *kernel_shape,
+                               conv_method method, const int *m, const conv_plan_options *opts,
+                               conv_plan_info *info) {
+    conv_plan_options d;
+    Geometry g;
+    return fc_fill_geometry_nd(nd, B, C, Cout, in_shape, kernel_shape, (int)method, m, &g, info,
+                               opts_or_default(opts, &d));
+}
+
 conv_status conv_plan_ex(conv_plan_t *out, int B, int C, int Cout, int H, int W, int r,
                          conv_method method, int m, conv_gemm_impl gemm) {
     conv_plan_options o;
@@ -672,11 +878,12 @@ conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, in
 
 void conv_destroy(conv_plan_t p) {
     if (!p) return;
-    if (p->d_consts || p->h2d || p->d2h) {
+    if (p->d_consts || p->d_nd || p->h2d || p->d2h) {
         int cur = -1;
         cudaGetDevice(&cur);
         if (cur != p->device) cudaSetDevice(p->device);
         if (p->d_consts) cudaFree(p->d_consts);
+        if (p->d_nd) cudaFree(p->d_nd);
         if (p->h2d) cudaStreamDestroy(p->h2d);
         if (p->d2h) cudaStreamDestroy(p->d2h);
         if (cur >= 0 && cur != p->device) cudaSetDevice(cur);
@@ -736,7 +943,7 @@ int conv_forward_launch_count(conv_plan_t p) {
     if (!p) return 0;
     if (p->g.method == CONV_DIRECT) return 1;
     // F16X3 FFT plans run a per-c' scale prologue before the z-sliced FFT kernel transform
-    const int nk1 = (p->g.vf16 && p->g.method != CONV_WINOGRAD && !p->generic_transforms) ? 2 : 1;
+    const int nk1 = p->generic_transforms ? 1 : fc_nk1_launches(p->g, p->g.vf16 ? 2 : 1);
     return nk1 + 3 * p->nchunks;
 }
 
@@ -804,6 +1011,20 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, cons
         g.vscale = (float *)(ws + p->off_vscale);
     }
     const int split = g.vf16 ? 2 : (Vlo != nullptr);
+    if (g.nd && stage != 2) {  // N-D / non-isotropic: the generic separable transforms
+        if (stage == 1 && g.vf16) {
+            conv_status st = launch_result(cudaMemsetAsync(g.umax, 0, sizeof(unsigned int) * (size_t)g.B, s),
+                                           "max|U_b| reset");
+            if (st) return st;
+        }
+        static const char *names[4] = {"NK1 kernel transform (N-D)", "NK2 input transform (N-D)", "",
+                                       "NK4 output transform (N-D)"};
+        if (stage == 0) return launch_result(fc_launch_nd_stage(g, p->d_nd, 0, w, V, Vlo, split, s), names[0]);
+        if (stage == 1) return launch_result(fc_launch_nd_stage(g, p->d_nd, 1, in, U, nullptr, 0, s), names[1]);
+        if (stage == 3) return launch_result(fc_launch_nd_stage(g, p->d_nd, 3, X, out, nullptr, 0, s), names[3]);
+        fc_set_error("bad stage %d", stage);
+        return CONV_ERR_INVALID_ARG;
+    }
     switch (stage) {
         case 0: {
             int handled = 0;
@@ -892,14 +1113,15 @@ static conv_status forward_impl(conv_plan_s *p, const float *in, const float *w,
     if (st) return st;
     const Geometry &g = p->g;
     if (g.method == CONV_DIRECT) {
-        st = launch_result(fc_launch_direct(g, in, w, out, s), "NK5 direct");
+        st = launch_result(g.nd ? fc_launch_nd_direct(g, in, w, out, s) : fc_launch_direct(g, in, w, out, s),
+                           "NK5 direct");
         return st ? st : mark(2);
     }
     if (!skip_nk1 && ((st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0)))) return st;
     for (int b0 = 0; b0 < g.B; b0 += p->chunk) {
         const Geometry gc = fc_chunk_geometry(g, g.B - b0 < p->chunk ? g.B - b0 : p->chunk);
-        const float *in_c = in + (size_t)b0 * g.C * g.H * g.W;
-        float *out_c = out + (size_t)b0 * g.Cout * g.Ho * g.Wo;
+        const float *in_c = in + (size_t)b0 * g.C * (size_t)g.vin;
+        float *out_c = out + (size_t)b0 * g.Cout * (size_t)g.vout;
         for (int k = 1; k < 4; ++k)
             if ((st = run_stage(p, gc, k, in_c, w, out_c, ws, s)) || (st = mark(k))) return st;
     }
@@ -1072,8 +1294,8 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
     if (st) return st;
     const Geometry &g = p->g;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t img_in = (size_t)g.C * g.H * g.W, img_out = (size_t)g.Cout * g.Ho * g.Wo;
-    const size_t nw = (size_t)g.Cout * g.C * g.r * g.r * 4;
+    const size_t img_in = (size_t)g.C * (size_t)g.vin, img_out = (size_t)g.Cout * (size_t)g.vout;
+    const size_t nw = (size_t)g.Cout * g.C * (size_t)g.kvol * 4;
     cudaError_t e = cudaMemcpyAsync(d_w, h_w, nw, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return launch_result(e, "H2D copy (weights)");
     if (g.method == CONV_DIRECT || !p->h2d || !p->d2h) {

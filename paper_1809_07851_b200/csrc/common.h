@@ -79,6 +79,22 @@ struct Geometry {
     // ("X at w = 2")
     int gc, Xz, Xm;
     int tc_1sm;  // conv_plan_options.single_cta_mma: single-CTA contraction tiles even when M > 128
+    // N-dimensional / non-isotropic layers (conv_plan_nd; "an arbitrary number of
+    // dimensions, as well as non-isotropic kernels"): nd = 0 for the 2-D isotropic plans above;
+    // nd = 1..3 runs the generic separable transforms of transforms_nd.cu.  Axis arrays are
+    // right-aligned in 3 slots (slot 2 = the last, fastest axis; unused leading slots hold 1).
+    int nd;
+    int ax_in[3], ax_r[3], ax_m[3], ax_t[3], ax_n[3], ax_o[3];
+    int ax_len[3];  // transformed length per axis: t, except the FFT's last axis t/2 + 1
+    long long vin, vout;  // input / output elements per (image, channel) plane or volume
+    int kvol;             // kernel elements per (c', c): r^2 (2-D) or prod r_d
+};
+
+// Per-axis constants of an N-D plan (fp64 -> fp32 once): Winograd B^T [t][t], G [t][r],
+// A^T [m][t] of F(m_d, r_d), and the twiddles cos / sin(2 pi j / t_d).
+struct NdConsts {
+    float BT[3][64], G[3][64], AT[3][64];
+    float cosv[3][FC_MAX_T], sinv[3][FC_MAX_T];
 };
 
 struct conv_plan_s {
@@ -88,6 +104,7 @@ struct conv_plan_s {
     ConvConsts host_consts;
     double AT64[64], BT64[64], G64[64];  // exact Winograd matrices (fp64)
     ConvConsts *d_consts;                 // device copy
+    NdConsts *d_nd;                       // N-D plans: per-axis constants (device)
     int generic_transforms;               // 1: force the runtime-t reference transform kernels
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
     size_t off_vscale, off_umax;          // F16X3: per-c' scales [2][Cout], per-image max|U| [B] (else 0)
@@ -174,7 +191,7 @@ __device__ __forceinline__ float fc_pow2_scale(float mx, int top);
 // Every thread of the block must call it (once per kernel).
 __device__ __forceinline__ float fc_row_vscale(const Geometry &g, const float *__restrict__ w, int co) {
     __shared__ float s_red[32];
-    const int len = g.C * g.r * g.r;
+    const int len = g.C * g.kvol;
     const float *row = w + (size_t)co * len;
     float mx = 0.f;
     // all loads of a round issued before any use (one memory round trip per 8 x blockDim x 4 floats)
@@ -252,6 +269,8 @@ conv_status fc_best_m(int B, int C, int Cout, int H, int W, int r, int method, c
                       int *m_out, double *model_ms, int max_cand, int *n_cand, int *cand_m, double *cand_ms);
 // 1 when (method, t, m, r) has compile-time-t NK2 / NK4 kernels (transforms_fast.cu)
 int fc_fast_transforms(int method, int t, int m, int r);
+// kernel launches NK1 issues (2 = F16X3 FFT codelets: per-c' scale prologue + transform)
+int fc_nk1_launches(const Geometry &g, int split);
 void fc_set_error(const char *fmt, ...);
 
 // ---- kernel launchers (return cudaGetLastError()) ----
@@ -270,6 +289,10 @@ cudaError_t fc_launch_gemm_tcgen05_f16(const Geometry &g, const void *Vhi, const
                                        const float *U, float *X, cudaStream_t s);
 cudaError_t fc_launch_direct(const Geometry &g, const float *in, const float *w, float *out,
                              cudaStream_t s);
+// N-D generic transforms (transforms_nd.cu): stage 0 = NK1, 1 = NK2, 3 = NK4; direct check path
+cudaError_t fc_launch_nd_stage(const Geometry &g, const NdConsts *dc, int stage, const float *src, float *dst,
+                               float *Vlo, int split, cudaStream_t s);
+cudaError_t fc_launch_nd_direct(const Geometry &g, const float *in, const float *w, float *out, cudaStream_t s);
 int fc_tcgen05_available();
 cudaError_t fc_init_twiddles();
 // FFT NK2 (forward) / NK4 transforms with compile-time t, split over fft_xforms_{a,b,c}.cu;

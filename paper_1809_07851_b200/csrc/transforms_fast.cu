@@ -615,3 +615,12 @@ int fc_fast_transforms(int method, int t, int m, int r) {
     }
     return 0;
 }
+
+// kernel launches of NK1 for this geometry: the FFT codelets with the F16X3 split run a
+// per-c' scale prologue first (2), everything else one kernel
+int fc_nk1_launches(const Geometry &g, int split) {
+    if (g.nd || g.method == CONV_WINOGRAD || g.method == CONV_DIRECT || split != 2) return 1;
+    if (g.r != 3 && g.r != 5) return 1;
+    if (g.r == 5 && g.t < 5) return 1;
+    return fc_fast_transforms(g.method, g.t, g.m, g.r) ? 2 : 1;
+}

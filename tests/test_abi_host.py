@@ -231,3 +231,30 @@ def test_best_m_model(lib):
         fc.best_m(1, 4, 4, 16, 16, 3, "direct")
     with pytest.raises(fc.ConvError):
         fc.plan_query(1, 4, 4, 16, 16, 3, "winograd", -1)
+
+
+def test_plan_query_nd_geometry(lib):
+    """conv_plan_query_nd: per-axis tiles t_d = m_d + r_d - 1, tiles per axis
+    ceil((n_d - r_d + 1) / m_d), E = prod t_d (Winograd) or prod_{d<nd-1} t_d (t_last/2 + 1)
+    (FFT half spectrum on the last axis), and the Table layer-stuff costs with volumes."""
+    B, C, Co = 2, 8, 16
+    q = fc.plan_query_nd(B, C, Co, (10, 12, 14), (3, 3, 3), "winograd", (2, 2, 4))
+    assert q["nd"] == 3 and list(q["t_shape"]) == [4, 4, 6] and list(q["tiles"]) == [4, 5, 3]
+    assert q["E"] == 4 * 4 * 6 and q["N"] == 60 and q["BN"] == B * 60
+    assert list(q["out_shape"]) == [8, 10, 12]
+    assert q["direct_flops"] == 2.0 * B * C * Co * 8 * 10 * 12 * 27
+    assert q["alg_bytes"][1] == pytest.approx(4 * B * C * 10 * 12 * 14 + 4 * q["E"] * B * C * 60)
+    f = fc.plan_query_nd(B, C, Co, (10, 12, 14), (3, 3, 3), "regular_fft", (6, 6, 6))
+    assert f["E"] == 8 * 8 * 5 and f["planes"] == 2
+    one = fc.plan_query_nd(B, C, Co, (30,), (5,), "gauss_fft", (10,))
+    assert one["nd"] == 1 and one["E"] == 14 // 2 + 1 and one["N"] == 3
+    # non-isotropic 2-D kernel (1 x 3): the r = 1 axis is an identity Winograd axis, t = m
+    ni = fc.plan_query_nd(B, C, Co, (9, 12), (1, 3), "winograd", (3, 4))
+    assert list(ni["t_shape"])[1:] == [3, 6] and ni["E"] == 18
+    # nd = 2, square kernel, equal tiles: the 2-D plan itself
+    assert fc.plan_query_nd(B, C, Co, (20, 20), (3, 3), "winograd", (4, 4))["E"] == \
+        fc.plan_query(B, C, Co, 20, 20, 3, "winograd", 4)["E"]
+    with pytest.raises(fc.ConvError):
+        fc.plan_query_nd(B, C, Co, (10, 12, 14), (3, 3, 3), "winograd", (2, 2, 7))  # t = 9 > 8
+    with pytest.raises(fc.ConvError):
+        fc.plan_query_nd(B, C, Co, (2, 12, 14), (3, 3, 3), "regular_fft", (2, 2, 2))  # input < kernel

@@ -151,3 +151,79 @@ def test_rejects_bad_shapes():
     I, W = synth.make_inputs(cfg)
     with pytest.raises(ValueError):
         oracle.conv_fp64_sampled(I, W, [[0, 0, 3, 0]])
+
+
+# ------------------------------------------------------------ N-D oracle ---
+# oracle.conv_nd_fp64 (P:926-929 N-dimensional / non-isotropic extension of Eq. 5)
+
+@pytest.mark.parametrize("ishape,wshape", [((2, 3, 17), (4, 3, 5)), ((2, 3, 9, 11, 8), (2, 3, 3, 2, 4)),
+                                           ((1, 2, 6, 5, 7), (3, 2, 1, 3, 2))])
+def test_nd_against_torch_convnd(ishape, wshape):
+    """torch's float64 conv1d / conv3d on CPU (an independent library routine)."""
+    g = torch.Generator().manual_seed(7)
+    I = torch.randn(ishape, generator=g)
+    W = torch.randn(wshape, generator=g)
+    O = oracle.conv_nd_fp64(I, W)
+    f = {3: torch.nn.functional.conv1d, 5: torch.nn.functional.conv3d}[len(ishape)]
+    R = f(I.double(), W.double()).numpy()
+    assert O.shape == R.shape
+    assert np.abs(O - R).max() <= 1e-12 * np.abs(R).max()
+
+
+def test_nd_fsum_bruteforce():
+    """Every fp32 product is exact in fp64: math.fsum of the products at sampled 3-D outputs
+    is the correctly rounded exact sum."""
+    rng = np.random.default_rng(3)
+    I = rng.standard_normal((2, 3, 7, 6, 9)).astype(np.float32)
+    W = rng.standard_normal((2, 3, 3, 2, 4)).astype(np.float32)
+    O = oracle.conv_nd_fp64(I, W)
+    for _ in range(64):
+        b, co = rng.integers(0, 2), rng.integers(0, 2)
+        i0, i1, i2 = rng.integers(0, 5), rng.integers(0, 5), rng.integers(0, 6)
+        terms = [float(I[b, c, i0 + p, i1 + q, i2 + s]) * float(W[co, c, p, q, s])
+                 for c in range(3) for p in range(3) for q in range(2) for s in range(4)]
+        assert abs(O[b, co, i0, i1, i2] - math.fsum(terms)) <= 1e-13 * max(1.0, max(abs(x) for x in terms))
+
+
+@pytest.mark.parametrize("tap", [(0, 0, 0), (1, 2, 0), (2, 0, 3)])
+def test_nd_delta_kernel_shifts_input(tap):
+    """W[c'][c] = delta_{c'c} delta_{p, tap}: O[b][c] is I[b][c] shifted by tap, exactly."""
+    I = _int_data((2, 3, 6, 7, 8), 11)
+    W = np.zeros((3, 3, 3, 3, 4), dtype=np.float32)
+    for c in range(3):
+        W[c, c][tap] = 1.0
+    O = oracle.conv_nd_fp64(I, W)
+    a, b_, c_ = tap
+    assert np.array_equal(O, I[:, :, a:a + 4, b_:b_ + 5, c_:c_ + 5].astype(np.float64))
+
+
+def test_nd_separable_kernel_closed_form():
+    """A rank-one kernel W = u (x) v (x) w (C = C' = 1) convolves axis by axis: three
+    successive 1-D valid correlations (numpy.correlate), exact on integer data."""
+    I = _int_data((1, 1, 7, 6, 9), 12)
+    u, v, w = np.array([1, -2, 3], np.float32), np.array([2, 1], np.float32), np.array([-1, 0, 2, 1], np.float32)
+    W = np.einsum("i,j,k->ijk", u, v, w).astype(np.float32)[None, None]
+    O = oracle.conv_nd_fp64(I, W)[0, 0]
+    x = I[0, 0].astype(np.float64)
+    x = np.apply_along_axis(lambda a: np.correlate(a, w, "valid"), 2, x)
+    x = np.apply_along_axis(lambda a: np.correlate(a, v, "valid"), 1, x)
+    x = np.apply_along_axis(lambda a: np.correlate(a, u, "valid"), 0, x)
+    assert np.array_equal(O, x)
+
+
+def test_nd_two_d_matches_the_2d_oracle():
+    """nd = 2 with a square kernel is Eq. 5 itself: bit-identical to oracle.conv_fp64 (same
+    (c, p, q) summation order), and a 1 x r kernel is the 1-D correlation of every row."""
+    I, W = synth.make_inputs(synth.custom(2, 3, 4, 9, 11, 3, seed=13, dist="normal"))
+    assert np.array_equal(oracle.conv_nd_fp64(I, W), oracle.conv_fp64(I, W))
+    I1 = _int_data((1, 1, 4, 9), 14)
+    k = np.array([3, -1, 2], np.float32)
+    O = oracle.conv_nd_fp64(I1, k.reshape(1, 1, 1, 3))[0, 0]
+    assert np.array_equal(O, np.stack([np.correlate(row.astype(np.float64), k, "valid") for row in I1[0, 0]]))
+
+
+def test_nd_rejects_bad_shapes():
+    with pytest.raises(ValueError):
+        oracle.conv_nd_fp64(np.zeros((1, 2, 3, 3, 3, 3), np.float32), np.zeros((1, 2, 1, 1, 1, 1), np.float32))
+    with pytest.raises(ValueError):
+        oracle.conv_nd_fp64(np.zeros((1, 2, 3), np.float32), np.zeros((1, 2, 4), np.float32))
