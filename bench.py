@@ -371,6 +371,9 @@ def main():
     ap.add_argument("--reference-budget-s", type=float, default=120.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the 3xTF32 arm, cached/graph runs, peaks")
+    ap.add_argument("--mode", default="batch", choices=["batch", "eshard"],
+                    help="batch-sharded ranks (no data-path collective) or element-sharded ranks "
+                         "(all-to-alls of U and X, SURVEY 8(f)3); eshard needs --method and --m")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -431,6 +434,12 @@ def main():
         torch.cuda.synchronize()
         total, _ = timer_fn.run(steps, lambda: plan.forward(x, w, out, ws))
         return total / steps
+
+    if args.mode == "eshard":
+        run_eshard(args, fc, parallel, base, gcfg, cfg, I_all_shape=None, x=x, w=w, dev=dev, stream=stream,
+                   timer_fn=timer_fn, job_flops=job_flops, rank=rank, world=world, oversub=oversub, clocks=clocks,
+                   nvml=nvml, flush=flush, io_bytes=io_bytes)
+        return
 
     # ---- sweep (the paper's rule: each method at its fastest m) -----------------
     runs = list(cfg.runs) if args.method == "auto" else [(args.method, args.m)]
@@ -612,6 +621,58 @@ def main():
             "gpu_launches_per_rank": plan.launches * args.steps,
         }
         line.update(extras)
+        print(json.dumps(line), flush=True)
+    parallel.barrier()
+
+
+def run_eshard(args, fc, parallel, base, gcfg, cfg, I_all_shape, x, w, dev, stream, timer_fn, job_flops, rank, world,
+               oversub, clocks, nvml, flush, io_bytes):
+    """Element-sharded mode: rank k owns the transformed elements
+    parallel.shard_range(E, k, N) of every image and the transforms of its own images; one
+    step = forward_a (NK1 on own elements, NK2, U pack) -> all-to-all U + all-gather of the
+    per-image maxima -> forward_b (NK3) -> all-to-all X -> forward_c (NK4), timed with CUDA
+    events around the whole step (collectives included), max over ranks."""
+    import torch
+    if args.method == "auto" or args.method == "direct":
+        raise SystemExit("--mode eshard needs --method winograd|regular_fft|gauss_fft and --m")
+    batch = [hi - lo for lo, hi in (parallel.shard_range(gcfg.B, k, world) for k in range(world))]
+    es = fc.EShard(world, rank, batch, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, args.method, args.m, args.gemm)
+    ws = es.alloc_workspace(dev)
+    out = torch.empty(es.out_shape, device=dev)
+    host = oversub or not torch.distributed.is_initialized() or torch.distributed.get_backend() != "nccl"
+    bufs = parallel.eshard_forward(es, x, w, out, ws, host_staging=host and world > 1)
+    for _ in range(args.warmup):
+        parallel.eshard_forward(es, x, w, out, ws, bufs, host_staging=host and world > 1)
+    torch.cuda.synchronize()
+    parallel.barrier()
+    t0 = time.time()
+    total, per = timer_fn.run(args.steps, lambda: parallel.eshard_forward(es, x, w, out, ws, bufs,
+                                                                          host_staging=host and world > 1))
+    torch.cuda.synchronize()
+    parallel.barrier()
+    t1 = time.time()
+    rank_ms = total / args.steps
+    ms = parallel.max_over_ranks(rank_ms, dev if not oversub else None)
+    per_rank = parallel.all_gather_scalar(rank_ms, dev if not oversub else None)
+    clk = nvml.merge(clocks.summary(t0, t1))
+    clocks.stop()
+    if rank == 0:
+        line = {"metric": METRIC, "value": job_flops / (ms * 1e-3) / 1e12, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "ms_per_step_stats": {"per_rank_ms": per_rank},
+                "config": {"workload": base.name, "global_batch": gcfg.B, "B_per_gpu": cfg.B, "C": cfg.C,
+                           "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": args.method, "m": args.m,
+                           "gemm": fc.GEMM_NAMES.get(es.info["gemm"], args.gemm),
+                           "parallelism": "es%d (element-sharded: elements [e0, e1) of every image per rank; "
+                                          "all-to-all of U and X, all-gather of per-image maxima%s)" % (
+                                              world, ", staged through the host (gloo)" if host and world > 1 else
+                                              ", NCCL" if world > 1 else ""),
+                           "elements_per_rank": es.e_count, "E": es.info["E"],
+                           "bytes_exchanged_per_rank": {"u_send": sum(es.u_send), "x_send": sum(es.x_send)},
+                           "l2": "flushed between steps" if flush else "no flush (%.0f MB/GPU)" % (io_bytes / 1e6),
+                           "oversubscribed": oversub},
+                "clocks": clk, "e2e": None, "gpu_launches": None}
         print(json.dumps(line), flush=True)
     parallel.barrier()
 

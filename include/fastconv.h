@@ -303,6 +303,42 @@ conv_status conv_graph_create(conv_plan_t p, const float *in, const float *w, fl
 conv_status conv_graph_launch(conv_graph_t g, void *stream);
 void conv_graph_destroy(conv_graph_t g);   /* NULL-safe */
 
+/* Element-sharded multi-GPU execution.  The contraction is E
+ * independent products X_e = V_e U_e, so rank j of `world` can own the
+ * transformed elements e in [e0_j, e1_j) (an even split of E) for every image while the
+ * transforms stay with the images: rank j transforms its batch[j] images (NK2 / NK4) and
+ * only its E_j / E share of the kernels (NK1), instead of every rank transforming and
+ * reading all of V as the batch-sharded plan does.  One forward is three calls with two
+ * all-to-alls (and one tiny all-gather) in between, done by the caller with its
+ * communicator (NCCL over NVLink in bench/parallel.py):
+ *   conv_eshard_forward_a  NK1 (own elements), NK2 (own images), U packed per peer into
+ *                          u_send (peer-major, u_send_bytes[k] to peer k), and this rank's
+ *                          per-image max|U_b| (F16X3 scale inputs) into umax_out[batch[rank]]
+ *   caller                 all-to-all u_send -> u_recv (u_recv_bytes[k] from peer k);
+ *                          all-gather umax_out -> umax_all[sum batch] in rank order
+ *   conv_eshard_forward_b  NK3 for own elements over every image's tiles; X packed per peer
+ *   caller                 all-to-all x_send -> x_recv
+ *   conv_eshard_forward_c  X chunks placed, NK4 for own images -> out[batch[rank]][C'][Ho][Wo]
+ * in [batch[rank]][C][H][W] and w [C'][C][r][r] on this rank's device.  Results equal
+ * conv_forward of the whole batch bit for bit (same per-column arithmetic).  Buffers are the
+ * caller's (device memory of the plan's device); sizes from conv_eshard_sizes (arrays of
+ * `world` entries, may be NULL).  NK1 uses the generic kernel (its element range).
+ * Errors: INVALID_ARG for bad rank/world/batch, the direct method, or short buffers;
+ * UNSUPPORTED when E < world. */
+typedef struct conv_eshard_s *conv_eshard_t;
+conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const int *batch, int C, int Cout, int H,
+                               int W, int r, conv_method method, int m, const conv_plan_options *opts);
+conv_status conv_eshard_sizes(conv_eshard_t e, size_t *workspace_bytes, size_t *u_send_bytes,
+                              size_t *u_recv_bytes, size_t *x_send_bytes, size_t *x_recv_bytes);
+conv_status conv_eshard_get_info(conv_eshard_t e, conv_plan_info *local_plan, int *e_lo, int *e_count);
+conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float *w, void *u_send, float *umax_out,
+                                  void *workspace, size_t workspace_bytes, void *stream);
+conv_status conv_eshard_forward_b(conv_eshard_t e, const void *u_recv, const float *umax_all, void *x_send,
+                                  void *workspace, size_t workspace_bytes, void *stream);
+conv_status conv_eshard_forward_c(conv_eshard_t e, const void *x_recv, float *out, void *workspace,
+                                  size_t workspace_bytes, void *stream);
+void conv_eshard_destroy(conv_eshard_t e);   /* NULL-safe */
+
 #ifdef __cplusplus
 }
 #endif

@@ -136,6 +136,14 @@ def load(build_if_missing: bool = False):
         "conv_graph_create": ([vp, vp, vp, vp, vp, sz, i, i, ctypes.POINTER(vp)], i),
         "conv_graph_launch": ([vp, vp], i),
         "conv_graph_destroy": ([vp], None),
+        "conv_eshard_create": ([ctypes.POINTER(vp), i, i, ctypes.POINTER(i)] + [i] * 7 +
+                               [ctypes.POINTER(PlanOptions)], i),
+        "conv_eshard_sizes": ([vp] + [ctypes.POINTER(sz)] * 5, i),
+        "conv_eshard_get_info": ([vp, ctypes.POINTER(PlanInfo), ctypes.POINTER(i), ctypes.POINTER(i)], i),
+        "conv_eshard_forward_a": ([vp, vp, vp, vp, vp, vp, sz, vp], i),
+        "conv_eshard_forward_b": ([vp, vp, vp, vp, vp, sz, vp], i),
+        "conv_eshard_forward_c": ([vp, vp, vp, vp, sz, vp], i),
+        "conv_eshard_destroy": ([vp], None),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)
@@ -354,6 +362,61 @@ class Plan:
         G = (ctypes.c_double * (t * r))()
         _check(load().conv_plan_winograd_matrices(self._h, AT, BT, G))
         return list(AT), list(BT), list(G)
+
+
+class EShard:
+    """conv_eshard_*: element-sharded forward of one rank.  Argument
+    marshalling only; parallel.eshard_forward runs the exchanges between the three calls."""
+
+    def __init__(self, world: int, rank: int, batch, C, Cout, H, W, r, method: str, m: int, gemm: str = "auto",
+                 **opts):
+        lib = load()
+        h = ctypes.c_void_p()
+        o = options(gemm, **opts)
+        ba = (ctypes.c_int * world)(*batch)
+        _check(lib.conv_eshard_create(ctypes.byref(h), world, rank, ba, C, Cout, H, W, r, METHODS[method], m,
+                                      ctypes.byref(o)))
+        self._h = h
+        self.world, self.rank, self.batch = world, rank, list(batch)
+        wsb = ctypes.c_size_t()
+        arrs = [(ctypes.c_size_t * world)() for _ in range(4)]
+        _check(lib.conv_eshard_sizes(h, ctypes.byref(wsb), *arrs))
+        self.workspace_bytes = int(wsb.value)
+        self.u_send, self.u_recv, self.x_send, self.x_recv = ([int(v) for v in a] for a in arrs)
+        info = PlanInfo()
+        elo, ecnt = ctypes.c_int(), ctypes.c_int()
+        _check(lib.conv_eshard_get_info(h, ctypes.byref(info), ctypes.byref(elo), ctypes.byref(ecnt)))
+        self.info = info.as_dict()
+        self.e_lo, self.e_count = elo.value, ecnt.value
+        B = batch[rank]
+        self.in_shape = (B, C, H, W)
+        self.w_shape = (Cout, C, r, r)
+        self.out_shape = (B, Cout, H - r + 1, W - r + 1)
+
+    def alloc_workspace(self, device=None) -> torch.Tensor:
+        return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device or "cuda")
+
+    def forward_a(self, x, w, u_send, umax_out, workspace, stream=None):
+        _check_tensor(x, "input", self.in_shape)
+        _check_tensor(w, "weights", self.w_shape)
+        _check(load().conv_eshard_forward_a(self._h, x.data_ptr(), w.data_ptr(), u_send.data_ptr(),
+                                            umax_out.data_ptr(), workspace.data_ptr(), _nbytes(workspace),
+                                            _stream_ptr(stream)))
+
+    def forward_b(self, u_recv, umax_all, x_send, workspace, stream=None):
+        _check(load().conv_eshard_forward_b(self._h, u_recv.data_ptr(), umax_all.data_ptr(), x_send.data_ptr(),
+                                            workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream)))
+
+    def forward_c(self, x_recv, out, workspace, stream=None):
+        _check_tensor(out, "out", self.out_shape)
+        _check(load().conv_eshard_forward_c(self._h, x_recv.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                            _nbytes(workspace), _stream_ptr(stream)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_eshard_destroy(h)
+            self._h = None
 
 
 class Graph:

@@ -372,6 +372,8 @@ static conv_status finish_geometry(Geometry &G, conv_plan_info *info, const conv
         }
     }
     G.tc_1sm = opts->single_cta_mma;
+    G.e_lo = 0;
+    G.e_hi = G.E;
     if (!info) return CONV_OK;
     conv_plan_info I;
     memset(&I, 0, sizeof(I));
@@ -1439,6 +1441,376 @@ conv_status conv_graph_launch(conv_graph_t gr, void *stream) {
         return CONV_ERR_DEVICE_MISMATCH;
     }
     return launch_result(cudaGraphLaunch(gr->exec, (cudaStream_t)stream), "graph launch");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Element-sharded execution (the contraction's E independent
+// products): rank j of g owns the transformed elements e in [e0_j, e1_j)
+// (parallel.shard_range over E) for EVERY image, and its own images b in [lo_j, hi_j) for
+// the transforms:
+//   a) NK1 for its elements only (V_j: E_j / E of V -- no replicated kernel transform),
+//      NK2 for its images (U_local, per-image max|U_b|), U packed per destination peer;
+//   -- caller: all-to-all of U (peer-major chunks) and all-gather of the per-image max|U_b|
+//   b) NK3 for its elements over all B N columns (the received chunks are one U operand
+//      [sum_k NB_k][Z_j][K][128]; F16X3 scales per column from the gathered maxima),
+//      X_j packed per destination peer (its images' columns);
+//   -- caller: all-to-all of X
+//   c) X chunks placed into X_local [Xz][Xm][BN_pad], NK4 for its images.
+// Every per-column computation is the one the batch-sharded / single-GPU plan performs
+// (same V entries, same K order, same per-image scale), so results are bit-identical to
+// conv_forward on the whole batch.
+// ---------------------------------------------------------------------------
+struct conv_eshard_s {
+    int world, rank;
+    std::vector<int> blo, bcnt;           // images per rank (prefix / count)
+    std::vector<int> elo, ecnt;           // elements per rank
+    std::vector<long long> bnpad;         // per rank: its images' B_k N columns padded to 128
+    long long bn_tot;                     // sum of bnpad
+    conv_plan_s *lp;                      // local plan: this rank's images, all E (NK2 / NK4)
+    conv_plan_s lpx;                      // the same plan with this workspace's U / X / max offsets
+    char *d_seg;                          // device table: per-peer column offset, B_k N, first image
+    Geometry gv;                          // NK1 over [e0, e1) (generic kernel, full-E indices)
+    Geometry gj;                          // NK3 on E_j elements, bn_tot columns (N = 1)
+    int pu, px;                           // plane groups of U / X (3 for Gauss three-plane, else 1)
+    size_t off_V, off_Vlo, off_vscale, off_umaxc, off_Xj, off_U, off_X, off_umaxl, ws_bytes;
+    std::vector<size_t> u_send, u_recv, x_send, x_recv;
+};
+
+static int split_lo(int n, int k, int w) { return k * (n / w) + (k < n % w ? k : n % w); }
+
+extern "C" {
+
+conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const int *batch, int C, int Cout, int H,
+                               int W, int r, conv_method method, int m, const conv_plan_options *opts_in) {
+    if (!out || !batch || world < 1 || rank < 0 || rank >= world || method == CONV_DIRECT) {
+        fc_set_error("conv_eshard_create: bad rank / world / batch or the direct method");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_plan_options opts;
+    if (opts_in) {
+        conv_status st = check_options(opts_in);
+        if (st) return st;
+        opts = *opts_in;
+    } else {
+        conv_plan_options_init(&opts);
+    }
+    opts.chunk_images = 0;
+    int Btot = 0;
+    for (int k = 0; k < world; ++k) {
+        if (batch[k] < 1) {
+            fc_set_error("conv_eshard_create: every rank needs >= 1 image (rank %d has %d)", k, batch[k]);
+            return CONV_ERR_INVALID_ARG;
+        }
+        Btot += batch[k];
+    }
+    conv_eshard_s *e = new (std::nothrow) conv_eshard_s();
+    if (!e) return CONV_ERR_OUT_OF_MEMORY;
+    e->world = world;
+    e->rank = rank;
+    conv_plan_t lp = nullptr;
+    conv_status st = plan_create(&lp, 0, batch[rank], C, Cout, H, W, r, method, m, nullptr, nullptr, nullptr, &opts);
+    if (st) {
+        delete e;
+        return st;
+    }
+    e->lp = lp;
+    const Geometry &g = lp->g;
+    if (g.E < world) {
+        conv_destroy(lp);
+        delete e;
+        fc_set_error("conv_eshard_create: %d elements cannot be split over %d ranks", g.E, world);
+        return CONV_ERR_UNSUPPORTED;
+    }
+    int acc = 0;
+    e->bn_tot = 0;
+    for (int k = 0; k < world; ++k) {
+        e->blo.push_back(acc);
+        e->bcnt.push_back(batch[k]);
+        acc += batch[k];
+        const long long bn = (long long)batch[k] * g.N;
+        e->bnpad.push_back((bn + FC_TB - 1) / FC_TB * FC_TB);
+        e->bn_tot += e->bnpad.back();
+        const int lo = split_lo(g.E, k, world), hi = split_lo(g.E, k + 1, world);
+        e->elo.push_back(lo);
+        e->ecnt.push_back(hi - lo);
+    }
+    e->pu = g.method == CONV_GAUSS_FFT ? 3 : 1;
+    e->px = (g.method == CONV_GAUSS_FFT && !g.gc) ? 3 : 1;
+    const int Ej = e->ecnt[rank];
+    // NK1 geometry: the generic kernel writes e in [e0, e1) relative to e0
+    e->gv = g;
+    e->gv.e_lo = e->elo[rank];
+    e->gv.e_hi = e->elo[rank] + Ej;
+    // NK3 geometry: E_j elements, every rank's (padded) columns, one "tile per image" so the
+    // F16X3 scale of column n is the per-column maximum built from the gathered per-image ones
+    Geometry gj = g;
+    gj.E = Ej;
+    gj.e_lo = 0;
+    gj.e_hi = Ej;
+    gj.Z = e->pu * Ej;
+    gj.Xz = g.gc ? Ej : gj.Z;
+    gj.B = (int)e->bn_tot;
+    gj.N = 1;
+    gj.divN = fc_fastdiv(1);
+    gj.BN = e->bn_tot;
+    gj.BN_pad = e->bn_tot;
+    e->gj = gj;
+    // workspace: V_j (hi, lo, scales), per-column maxima, X_j, then the local U / X / max|U_b|
+    const size_t vb = fc_v_bytes(gj);
+    size_t off = 0;
+    e->off_V = off;
+    off += align256(vb);
+    e->off_Vlo = lp->gemm == CONV_GEMM_FFMA ? 0 : off;
+    if (lp->gemm != CONV_GEMM_FFMA) off += align256(vb);
+    e->off_vscale = off;
+    off += align256((size_t)2 * Cout * 4);
+    e->off_umaxc = off;
+    off += align256((size_t)e->bn_tot * 4);
+    e->off_Xj = off;
+    off += align256((size_t)gj.Xz * gj.Xm * e->bn_tot * 4);
+    e->off_U = off;
+    off += align256(lp->info.bytes_U);
+    e->off_X = off;
+    off += align256(lp->info.bytes_X);
+    e->off_umaxl = off;
+    off += align256((size_t)batch[rank] * 4);
+    e->ws_bytes = off;
+    e->lpx = *lp;
+    e->lpx.off_U = e->off_U;
+    e->lpx.off_X = e->off_X;
+    e->lpx.off_umax = e->off_umaxl;
+    {  // per-peer segments of the contraction's columns (for the per-column F16X3 maxima)
+        std::vector<char> host((size_t)world * 20);
+        long long c0 = 0;
+        for (int k = 0; k < world; ++k) {
+            const long long bn = (long long)batch[k] * g.N;
+            memcpy(host.data() + (size_t)k * 8, &c0, 8);
+            memcpy(host.data() + (size_t)world * 8 + (size_t)k * 8, &bn, 8);
+            memcpy(host.data() + (size_t)world * 16 + (size_t)k * 4, &e->blo[k], 4);
+            c0 += e->bnpad[k];
+        }
+        cudaError_t ce = cudaMalloc(&e->d_seg, host.size());
+        if (ce == cudaSuccess) ce = cudaMemcpy(e->d_seg, host.data(), host.size(), cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) {
+            if (e->d_seg) cudaFree(e->d_seg);
+            conv_destroy(lp);
+            delete e;
+            fc_set_error("e-shard segment table: %s", cudaGetErrorString(ce));
+            return CONV_ERR_CUDA;
+        }
+    }
+    // per-peer message sizes (bytes)
+    const long long NBme = e->bnpad[rank] / FC_TB;
+    for (int k = 0; k < world; ++k) {
+        e->u_send.push_back((size_t)NBme * e->pu * e->ecnt[k] * g.K * FC_TB * 4);
+        e->u_recv.push_back((size_t)(e->bnpad[k] / FC_TB) * e->pu * Ej * g.K * FC_TB * 4);
+        e->x_send.push_back((size_t)e->px * Ej * g.Xm * e->bnpad[k] * 4);
+        e->x_recv.push_back((size_t)e->px * e->ecnt[k] * g.Xm * e->bnpad[rank] * 4);
+    }
+    *out = e;
+    return CONV_OK;
+}
+
+void conv_eshard_destroy(conv_eshard_t e) {
+    if (!e) return;
+    if (e->d_seg) cudaFree(e->d_seg);
+    conv_destroy(e->lp);
+    delete e;
+}
+
+conv_status conv_eshard_sizes(conv_eshard_t e, size_t *workspace_bytes, size_t *u_send, size_t *u_recv,
+                              size_t *x_send, size_t *x_recv) {
+    if (!e) {
+        fc_set_error("NULL e-shard plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (workspace_bytes) *workspace_bytes = e->ws_bytes;
+    for (int k = 0; k < e->world; ++k) {
+        if (u_send) u_send[k] = e->u_send[k];
+        if (u_recv) u_recv[k] = e->u_recv[k];
+        if (x_send) x_send[k] = e->x_send[k];
+        if (x_recv) x_recv[k] = e->x_recv[k];
+    }
+    return CONV_OK;
+}
+
+conv_status conv_eshard_get_info(conv_eshard_t e, conv_plan_info *local, int *e_lo, int *e_count) {
+    if (!e) {
+        fc_set_error("NULL e-shard plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (local) *local = e->lp->info;
+    if (e_lo) *e_lo = e->elo[e->rank];
+    if (e_count) *e_count = e->ecnt[e->rank];
+    return CONV_OK;
+}
+
+static conv_status eshard_check(conv_eshard_s *e, void *ws, size_t ws_bytes) {
+    if (!e) {
+        fc_set_error("NULL e-shard plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_status st = check_device(e->lp);
+    if (st) return st;
+    if (ws_bytes < e->ws_bytes) {
+        fc_set_error("workspace %zu bytes < required %zu", ws_bytes, e->ws_bytes);
+        return CONV_ERR_INVALID_ARG;
+    }
+    return check_dev_ptr(e->lp, ws, "workspace");
+}
+
+conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float *w, void *u_send, float *umax_out,
+                                  void *ws, size_t ws_bytes, void *stream) {
+    conv_status st = eshard_check(e, ws, ws_bytes);
+    if (st) return st;
+    if ((st = check_dev_ptr(e->lp, in, "in")) || (st = check_dev_ptr(e->lp, w, "weights")) ||
+        (st = check_dev_ptr(e->lp, u_send, "u_send")))
+        return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *b = (char *)ws;
+    conv_plan_s *lp = e->lp;
+    // NK1 for this rank's elements (generic kernel with the element range)
+    Geometry gv = e->gv;
+    gv.vscale = (float *)(b + e->off_vscale);
+    gv.umax = nullptr;
+    const int split = gv.vf16 ? 2 : (e->off_Vlo ? 1 : 0);
+    {  // the same NK1 kernel the whole-batch plan runs (codelet or generic), on the element range
+        float *Vj = (float *)(b + e->off_V), *Vjlo = e->off_Vlo ? (float *)(b + e->off_Vlo) : nullptr;
+        int handled = 0;
+        cudaError_t ce = cudaSuccess;
+        if (!lp->generic_transforms)
+            ce = fc_launch_kernel_transform_fast(gv, lp->host_consts, w, Vj, Vjlo, split, s, &handled);
+        if (!handled) ce = fc_launch_kernel_transform(gv, lp->d_consts, w, Vj, Vjlo, split, s);
+        if ((st = launch_result(ce, "NK1 kernel transform (element shard)"))) return st;
+    }
+    // NK2 for this rank's images into U_local (per-image maxima into the local slot)
+    if ((st = run_stage(&e->lpx, lp->g, 1, in, nullptr, nullptr, b, s))) return st;
+    if (umax_out) {
+        if ((st = check_dev_ptr(lp, umax_out, "umax_out"))) return st;
+        if (lp->g.vf16)
+            st = launch_result(cudaMemcpyAsync(umax_out, b + e->off_umaxl, (size_t)lp->g.B * 4,
+                                               cudaMemcpyDeviceToDevice, s), "max|U_b| copy");
+        else
+            st = launch_result(cudaMemsetAsync(umax_out, 0, (size_t)lp->g.B * 4, s), "max|U_b| clear");
+        if (st) return st;
+    }
+    // pack U_local [NB][Z][K][128] -> peer j: [NB][pu][E_j][K][128]
+    const Geometry &g = lp->g;
+    const size_t row = (size_t)g.K * FC_TB * 4;  // one (z) slab of a 128-tile block
+    const long long NB = e->bnpad[e->rank] / FC_TB;
+    char *dst = (char *)u_send;
+    for (int j = 0; j < e->world; ++j) {
+        const int Ej = e->ecnt[j];
+        for (int p = 0; p < e->pu; ++p) {
+            const char *src = b + e->off_U + (size_t)(p * g.E + e->elo[j]) * row;
+            st = launch_result(cudaMemcpy2DAsync(dst + (size_t)p * Ej * row, (size_t)e->pu * Ej * row, src,
+                                                 (size_t)g.Z * row, (size_t)Ej * row, (size_t)NB,
+                                                 cudaMemcpyDeviceToDevice, s),
+                               "U pack");
+            if (st) return st;
+        }
+        dst += e->u_send[j];
+    }
+    return CONV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// per-column F16X3 maxima of the element shard's contraction: column n of peer k's segment
+// (offset off_k) is tile n - off_k of peer k's images, image lo_k + (n - off_k) / N
+__global__ void eshard_col_umax(unsigned int *col, const unsigned int *img, const long long *seg_off,
+                                const int *seg_lo, const long long *seg_bn, int world, int N, long long total) {
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < total;
+         n += (long long)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k + 1 < world && n >= seg_off[k + 1]) ++k;
+        const long long t = n - seg_off[k];
+        col[n] = t < seg_bn[k] ? img[seg_lo[k] + (int)(t / N)] : 0u;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+conv_status conv_eshard_forward_b(conv_eshard_t e, const void *u_recv, const float *umax_all, void *x_send, void *ws,
+                                  size_t ws_bytes, void *stream) {
+    conv_status st = eshard_check(e, ws, ws_bytes);
+    if (st) return st;
+    if ((st = check_dev_ptr(e->lp, u_recv, "u_recv")) || (st = check_dev_ptr(e->lp, x_send, "x_send"))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *b = (char *)ws;
+    conv_plan_s *lp = e->lp;
+    Geometry gj = e->gj;
+    gj.vscale = (float *)(b + e->off_vscale);
+    gj.umax = nullptr;
+    float *V = (float *)(b + e->off_V);
+    float *Vlo = e->off_Vlo ? (float *)(b + e->off_Vlo) : nullptr;
+    float *Xj = (float *)(b + e->off_Xj);
+    const float *U = (const float *)u_recv;
+    if (gj.vf16) {
+        if (!umax_all || (st = check_dev_ptr(lp, umax_all, "umax_all"))) {
+            if (!st) fc_set_error("F16X3 element shards need the gathered per-image max|U_b|");
+            return st ? st : CONV_ERR_INVALID_ARG;
+        }
+        const int w = e->world;
+        const char *dtab = e->d_seg;
+        unsigned int *col = (unsigned int *)(b + e->off_umaxc);
+        const long long total = e->bn_tot;
+        eshard_col_umax<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+            col, (const unsigned int *)umax_all, (const long long *)dtab, (const int *)(dtab + (size_t)w * 16),
+            (const long long *)(dtab + (size_t)w * 8), w, lp->g.N, total);
+        if ((st = launch_result(cudaGetLastError(), "per-column maxima"))) return st;
+        gj.umax = col;
+    }
+    if (lp->gemm == CONV_GEMM_FFMA)
+        st = launch_result(fc_launch_gemm_ffma(gj, V, U, Xj, s), "NK3 FFMA contraction (element shard)");
+    else if (gj.vf16)
+        st = launch_result(fc_launch_gemm_tcgen05_f16(gj, V, Vlo, U, Xj, s), "NK3 F16X3 contraction (element shard)");
+    else
+        st = launch_result(fc_launch_gemm_tcgen05(gj, V, Vlo, U, Xj, s), "NK3 3xTF32 contraction (element shard)");
+    if (st) return st;
+    // pack X_j [Xz_j][Xm][bn_tot] -> peer k: [Xz_j][Xm][bnpad_k] (its images' columns)
+    char *dst = (char *)x_send;
+    long long col0 = 0;
+    for (int k = 0; k < e->world; ++k) {
+        const size_t wbytes = (size_t)e->bnpad[k] * 4;
+        st = launch_result(cudaMemcpy2DAsync(dst, wbytes, (const char *)Xj + col0 * 4, (size_t)e->bn_tot * 4, wbytes,
+                                             (size_t)gj.Xz * gj.Xm, cudaMemcpyDeviceToDevice, s),
+                           "X pack");
+        if (st) return st;
+        dst += e->x_send[k];
+        col0 += e->bnpad[k];
+    }
+    return CONV_OK;
+}
+
+conv_status conv_eshard_forward_c(conv_eshard_t e, const void *x_recv, float *out, void *ws, size_t ws_bytes,
+                                  void *stream) {
+    conv_status st = eshard_check(e, ws, ws_bytes);
+    if (st) return st;
+    if ((st = check_dev_ptr(e->lp, x_recv, "x_recv")) || (st = check_dev_ptr(e->lp, out, "out"))) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *b = (char *)ws;
+    conv_plan_s *lp = e->lp;
+    const Geometry &g = lp->g;
+    // peer j's chunk [px][E_j][Xm][BN_me] -> X_local rows (p E + e0_j ..) of [Xz][Xm][BN_me]
+    const size_t slab = (size_t)g.Xm * g.BN_pad * 4;  // one element plane of X_local
+    const char *src = (const char *)x_recv;
+    for (int j = 0; j < e->world; ++j) {
+        const int Ej = e->ecnt[j];
+        for (int p = 0; p < e->px; ++p) {
+            st = launch_result(cudaMemcpyAsync(b + e->off_X + (size_t)(p * g.E + e->elo[j]) * slab,
+                                               src + (size_t)p * Ej * slab, (size_t)Ej * slab,
+                                               cudaMemcpyDeviceToDevice, s),
+                               "X unpack");
+            if (st) return st;
+        }
+        src += e->x_recv[j];
+    }
+    return run_stage(&e->lpx, g, 3, nullptr, nullptr, out, b, s);
 }
 
 }  // extern "C"

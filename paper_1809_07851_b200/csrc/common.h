@@ -88,6 +88,9 @@ struct Geometry {
     int ax_len[3];  // transformed length per axis: t, except the FFT's last axis t/2 + 1
     long long vin, vout;  // input / output elements per (image, channel) plane or volume
     int kvol;             // kernel elements per (c', c): r^2 (2-D) or prod r_d
+    // element-sharded execution (conv_eshard_*): the generic NK1 writes only the transformed
+    // elements e in [e_lo, e_hi), at z relative to e_lo (V of E' = e_hi - e_lo elements)
+    int e_lo, e_hi;
 };
 
 // Per-axis constants of an N-D plan (fp64 -> fp32 once): Winograd B^T [t][t], G [t][r],

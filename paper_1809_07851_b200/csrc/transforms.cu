@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                                                             const float *__restrict__ w, float *__restrict__ V,
                                                             float *__restrict__ Vlo, int split) {
     __shared__ float s_cos[FC_MAX_T], s_sin[FC_MAX_T], s_G[64];
-    const int t = g.t, r = g.r, h = g.h, E = g.E;
+    const int t = g.t, r = g.r, h = g.h;
     for (int i = threadIdx.x; i < FC_MAX_T; i += blockDim.x) {
         s_cos[i] = cc->cosv[i];
         s_sin[i] = cc->sinv[i];
@@ -48,6 +48,9 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
         cstep = g.C;
     }
     const size_t zstride = (size_t)(g.cplx ? g.Cout : g.M) * g.Kp;
+    // element range [e_lo, e_hi) (element-sharded plans; the whole E otherwise): z relative to
+    // e_lo, plane groups of Er = e_hi - e_lo elements
+    const int elo = g.e_lo, ehi = g.e_hi, Er = ehi - elo;
     for (int c = c0; c < g.C; c += cstep) {
     const float *ker = w + ((size_t)co * g.C + c) * r * r;
     auto store = [&](int z, int row, int col, float v) {
@@ -62,9 +65,11 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                 T[p] = a;
             }
             for (int k = 0; k < t; ++k) {  // V[k][l] = sum_p G[k][p] T[p]
+                const int e = k * t + l;
+                if (e < elo || e >= ehi) continue;
                 float a = 0.f;
                 for (int p = 0; p < r; ++p) a = fmaf(s_G[k * r + p], T[p], a);
-                store(k * t + l, co, c, a);
+                store(e - elo, co, c, a);
             }
         }
         continue;
@@ -87,6 +92,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
             Ti[p] = ai;
         }
         for (int k = 0; k < t; ++k) {  // column DFT along p
+            if (k * h + l < elo || k * h + l >= ehi) continue;
             float ar = 0.f, ai = 0.f;
             int ph = 0;
             for (int p = 0; p < r; ++p) {
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                 if (ph >= t) ph -= t;
             }
             const float vr = ar * inv, vi = -ai * inv;  // conj(DFT) / t^2
-            const int e = k * h + l;
+            const int e = k * h + l - elo;
             if (g.method == CONV_REGULAR_FFT && g.cplx) {  // (V_r, V_i) planes
                 store(2 * e, co, c, vr);
                 store(2 * e + 1, co, c, vi);
@@ -109,8 +115,8 @@ __global__ void __launch_bounds__(256) nk1_kernel_transform(Geometry g, const Co
                 store(e, g.Cout + co, g.C + c, vr);
             } else {  // Gauss: V_r, V_i - V_r, V_r + V_i
                 store(e, co, c, vr);
-                store(E + e, co, c, vi - vr);
-                store(2 * E + e, co, c, vr + vi);
+                store(Er + e, co, c, vi - vr);
+                store(2 * Er + e, co, c, vr + vi);
             }
         }
     }

@@ -93,10 +93,12 @@ __global__ void __launch_bounds__(256) nk1_wino(Geometry g, const float *__restr
 #pragma unroll
                 for (int p = 0; p < R; ++p) s[j] = wtab::cfma(tg.G[kk][p], tmp[j][p][l], s[j]);
             }
+            const int e = kk * T + l - g.e_lo;  // element shards: [e_lo, e_hi) relative to e_lo
+            if (e < 0 || e >= g.e_hi - g.e_lo) continue;
             if (NC == 2)
-                fc_store_v2(V, Vlo, off + (size_t)(kk * T + l) * zstride, s[0], s[NC - 1], sv);
+                fc_store_v2(V, Vlo, off + (size_t)e * zstride, s[0], s[NC - 1], sv);
             else
-                fc_store_v(V, Vlo, off + (size_t)(kk * T + l) * zstride, s[0], split, sv);
+                fc_store_v(V, Vlo, off + (size_t)e * zstride, s[0], split, sv);
         }
 }
 template <int T, int R>
@@ -412,12 +414,15 @@ __global__ void __launch_bounds__(128) nk1_fft(Geometry g, const float *__restri
     // 64-bit add per kk instead of 64-bit index products per store)
     size_t hz = (size_t)H * zstride;
     asm("" : "+l"(hz));
-    size_t ez = (size_t)l * zstride;
+    // element shards write e in [e_lo, e_hi) relative to e_lo (the whole E otherwise)
+    const int elo = g.e_lo, ecnt = g.e_hi - g.e_lo;
+    size_t ez = (size_t)(l - elo) * zstride;
     const size_t o00 = (size_t)co * g.Kp + c;                          // (c', c)
     const size_t o01 = o00 + g.C, o10 = o00 + (size_t)g.Cout * g.Kp;  // (c', C + c), (C' + c', c)
-    const size_t o11 = o10 + g.C, gpl = (size_t)g.E * zstride;
+    const size_t o11 = o10 + g.C, gpl = (size_t)ecnt * zstride;
 #pragma unroll
     for (int kk = 0; kk < T; ++kk, ez += hz) {
+        if ((unsigned)(kk * H + l - elo) >= (unsigned)ecnt) continue;
         float vr[NC], vi[NC], t0[NC], t1[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {

@@ -1,10 +1,17 @@
-"""Batch-sharded multi-GPU execution: one process per GPU, each
-rank runs the whole four-stage pipeline on its own images and transforms the
-kernels locally.  There is NO collective on the data path -- the only
-torch.distributed calls are the untimed barrier, the max-over-ranks reduction of
-the timing, and (for parity checks) an all_gather of outputs outside the timed
-region.  The layer's images are independent units (Eq. 5 has no cross-b term,
-P:358-370), so sharding the batch changes no arithmetic."""
+"""Multi-GPU execution, one process per GPU.
+
+Batch-sharded: each rank runs the whole four-stage pipeline on its
+own images and transforms the kernels locally.  There is NO collective on the data
+path -- the only torch.distributed calls are the untimed barrier, the max-over-ranks
+reduction of the timing, and (for parity checks) an all_gather of outputs outside the
+timed region.  The layer's images are independent units (Eq. 5 has no cross-b term,
+P:358-370), and every per-image quantity (including the F16X3 per-image U scale) is
+computed per image, so sharding the batch changes no arithmetic.
+
+Element-sharded (``eshard_forward``): the contraction's E
+products are independent; rank j owns elements [e0_j, e1_j) of every
+image and only those kernel transforms, with one all-to-all of U and one of X (the
+real exchange steps -- NCCL over NVLink on a multi-GPU box)."""
 from __future__ import annotations
 
 import os
@@ -91,3 +98,50 @@ def gather_batch(local: torch.Tensor, B: int, world: int) -> torch.Tensor:
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad)
     return torch.cat([bufs[r][:hi - lo] for r, (lo, hi) in enumerate(sizes)], dim=0)
+
+
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_split, in_split, host_staging: bool):
+    """all_to_all_single on byte tensors; host_staging: through CPU copies (gloo)."""
+    if host_staging:
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, inp.cpu(), list(out_split), list(in_split))
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, list(out_split), list(in_split))
+
+
+def eshard_forward(es, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, ws: torch.Tensor,
+                   bufs: dict | None = None, host_staging: bool = False) -> dict:
+    """One element-sharded forward of this rank (``es``: a paper_1809_07851_b200.EShard):
+    conv_eshard_forward_a -> all-to-all U + all-gather max|U_b| -> forward_b -> all-to-all X
+    -> forward_c.  Returns the exchange buffers (reusable through ``bufs``)."""
+    dev = x.device
+    if bufs is None:
+        bufs = {"u_send": torch.empty(max(1, sum(es.u_send)), dtype=torch.uint8, device=dev),
+                "u_recv": torch.empty(max(1, sum(es.u_recv)), dtype=torch.uint8, device=dev),
+                "x_send": torch.empty(max(1, sum(es.x_send)), dtype=torch.uint8, device=dev),
+                "x_recv": torch.empty(max(1, sum(es.x_recv)), dtype=torch.uint8, device=dev),
+                "umax": torch.zeros(max(es.batch), dtype=torch.float32, device=dev),
+                "umax_all": torch.zeros(sum(es.batch), dtype=torch.float32, device=dev)}
+    es.forward_a(x, w, bufs["u_send"], bufs["umax"], ws)
+    world = es.world
+    if world > 1:
+        _a2a(bufs["u_recv"][:sum(es.u_recv)], bufs["u_send"][:sum(es.u_send)], es.u_recv, es.u_send, host_staging)
+        parts = [torch.zeros_like(bufs["umax"]) for _ in range(world)]
+        if host_staging:
+            cp = [p.cpu() for p in parts]
+            dist.all_gather(cp, bufs["umax"].cpu())
+            parts = [p.to(dev) for p in cp]
+        else:
+            dist.all_gather(parts, bufs["umax"])
+        bufs["umax_all"].copy_(torch.cat([parts[k][:es.batch[k]] for k in range(world)]))
+    else:
+        bufs["u_recv"][:sum(es.u_recv)].copy_(bufs["u_send"][:sum(es.u_send)])
+        bufs["umax_all"].copy_(bufs["umax"][:es.batch[0]])
+    es.forward_b(bufs["u_recv"], bufs["umax_all"], bufs["x_send"], ws)
+    if world > 1:
+        _a2a(bufs["x_recv"][:sum(es.x_recv)], bufs["x_send"][:sum(es.x_send)], es.x_recv, es.x_send, host_staging)
+    else:
+        bufs["x_recv"][:sum(es.x_recv)].copy_(bufs["x_send"][:sum(es.x_send)])
+    es.forward_c(bufs["x_recv"], out, ws)
+    return bufs

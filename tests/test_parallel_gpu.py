@@ -112,3 +112,91 @@ def test_bench_two_ranks_dry_run():
     assert d["config"]["oversubscribed"] == (torch.cuda.device_count() < 2)
     assert len(d["ms_per_step_stats"]["per_rank_ms"]) == 2
     assert d["ms_per_step"] == pytest.approx(max(d["ms_per_step_stats"]["per_rank_ms"]))
+
+
+ES_RUNS = [("winograd", 4, {}), ("regular_fft", 6, {}), ("regular_fft", 6, {"complex_mode": 0}),
+           ("gauss_fft", 8, {"gauss_combine": 0}), ("gauss_fft", 8, {"gauss_combine": 1})]
+
+
+def _es_worker(rank, world, port, shape, batch, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import synth
+    import paper_1809_07851_b200 as fc
+    from paper_1809_07851_b200 import parallel
+    try:
+        if world > 1:
+            parallel.init("gloo")
+        torch.cuda.set_device(0)
+        fc.load()
+        cfg = synth.custom(*shape, seed=131, dist="normal")
+        I, W = synth.make_inputs(cfg)
+        lo = sum(batch[:rank])
+        x, w = I[lo:lo + batch[rank]].contiguous().cuda(), W.cuda()
+        res = {}
+        for gemm in ("auto", "tcgen05", "ffma"):
+            for method, m, opts in ES_RUNS:
+                es = fc.EShard(world, rank, batch, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm, **opts)
+                ws = es.alloc_workspace()
+                y = torch.empty(es.out_shape, device="cuda")
+                parallel.eshard_forward(es, x, w, y, ws, host_staging=True)
+                torch.cuda.synchronize()
+                ref = fc.Plan(batch[rank], cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm,
+                              **opts).forward(x, w)
+                # the whole batch on one plan, this rank's images
+                full = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm, **opts).forward(
+                    I.cuda(), w)[lo:lo + batch[rank]]
+                res["%s/%s/m=%d/%s" % (gemm, method, m, opts)] = (bool(torch.equal(y, full)),
+                                                                  bool(torch.equal(ref, full)))
+        q.put((rank, res))
+    except Exception as exc:
+        q.put((rank, {"error": repr(exc)}))
+        raise
+    finally:
+        if torch.distributed.is_initialized():
+            torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,batch", [((5, 32, 256, 18, 18, 3), (3, 2)), ((4, 24, 64, 20, 17, 3), (1, 3)),
+                                         ((3, 16, 32, 14, 14, 3), (3,))])
+def test_element_sharded_equals_unsharded(shape, batch):
+    """element-sharded forwards (rank j: elements [e0_j, e1_j) of every image,
+    the transforms of its own images; all-to-alls of U and X) give each rank's images exactly
+    the unsharded forward's output -- every contraction mode and method, complex mode on
+    and off, Gauss three-plane and combined."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    world = len(batch)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_es_worker, args=(r, world, port, shape, batch, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, res in results:
+        assert "error" not in res, (rank, res)
+        bad = [k for k, (ok, _) in res.items() if not ok]
+        assert not bad, (rank, bad)
+    assert all(p.exitcode == 0 for p in procs)
+
+
+@pytest.mark.parametrize("gpus", [1, 2])
+def test_bench_eshard_mode(gpus):
+    """bench.py --mode eshard prints one line per run: deep layer, FFT m = 14,
+    element shards of E = 144 over the ranks."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    res = subprocess.run([sys.executable, "bench.py", "--gpus", str(gpus), "--steps", "3", "--warmup", "3",
+                          "--workload", "deep", "--mode", "eshard", "--method", "regular_fft", "--m", "14",
+                          "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, res.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == gpus and d["value"] > 0 and d["config"]["parallelism"].startswith("es%d" % gpus)
+    assert d["config"]["E"] == 144 and d["config"]["elements_per_rank"] == 144 // gpus
