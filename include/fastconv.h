@@ -303,6 +303,25 @@ conv_status conv_graph_create(conv_plan_t p, const float *in, const float *w, fl
 conv_status conv_graph_launch(conv_graph_t g, void *stream);
 void conv_graph_destroy(conv_graph_t g);   /* NULL-safe */
 
+/* Backward passes (not in the paper).  Both gradients of Eq. 5 are
+ * valid cross-correlations and run through the same fast pipeline after a re-layout:
+ *   which = 1  conv_backward_data:   dx[b][c][y][x] = sum_{c',p,q} dy[b][c'][y-p][x-q] w[c'][c][p][q]
+ *              (forward of the (r-1)-zero-padded dy [B][C'][H+r-1][W+r-1] with the flipped,
+ *              channel-transposed kernel; method / m as for conv_plan, m = 0: the planner's)
+ *   which = 2  conv_backward_filter: dw[c'][c][p][q] = sum_{b,i,j} dy[b][c'][i][j] x[b][c][i+p][j+q]
+ *              (forward of x with images and channels swapped against dy as an Ho x Wo kernel:
+ *              FFT tiles of the whole image, t = H, W <= 64, or CONV_DIRECT; m is ignored;
+ *              Winograd -> UNSUPPORTED)
+ * dy [B][C'][H-r+1][W-r+1], w [C'][C][r][r], x / dx [B][C][H][W], dw [C'][C][r][r], all
+ * device memory; the workspace holds the re-laid-out operands and the inner forward's
+ * U / V / X (conv_workspace_bytes).  Backward plans work only with these two calls. */
+conv_status conv_plan_backward(conv_plan_t *out, int which, int B, int C, int Cout, int H, int W, int r,
+                               conv_method method, int m, const conv_plan_options *opts);
+conv_status conv_backward_data(conv_plan_t p, const float *dy, const float *w, float *dx, void *workspace,
+                               size_t workspace_bytes, void *stream);
+conv_status conv_backward_filter(conv_plan_t p, const float *x, const float *dy, float *dw, void *workspace,
+                                 size_t workspace_bytes, void *stream);
+
 /* Element-sharded multi-GPU execution.  The contraction is E
  * independent products X_e = V_e U_e, so rank j of `world` can own the
  * transformed elements e in [e0_j, e1_j) (an even split of E) for every image while the

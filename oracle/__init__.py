@@ -49,6 +49,9 @@ def _load():
         ip = ctypes.POINTER(ctypes.c_int)
         lib.oracle_conv_nd_fp64.argtypes = [f32p, f32p, f64p] + [ctypes.c_int] * 4 + [ip, ip]
         lib.oracle_conv_nd_fp64.restype = ctypes.c_int
+        for fn in ("oracle_conv_bwd_data_fp64", "oracle_conv_bwd_filter_fp64"):
+            getattr(lib, fn).argtypes = [f32p, f32p, f64p] + [ctypes.c_int] * 6
+            getattr(lib, fn).restype = ctypes.c_int
         lib.oracle_num_threads.argtypes = []
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
@@ -129,6 +132,40 @@ def conv_nd_fp64(I, W) -> np.ndarray:
     if rc != 0:
         raise ValueError("oracle_conv_nd_fp64 rejected the shape")
     return O
+
+
+def conv_bwd_data_fp64(dY, W, H: int, Wd: int) -> np.ndarray:
+    """dX[b][c][y][x] = sum_{c',p,q} dY[b][c'][y-p][x-q] W[c'][c][p][q] (the adjoint of Eq. 5
+    in I) in fp64; dY [B][C'][H-r+1][W-r+1], W [C'][C][r][r] float32 -> [B][C][H][W]."""
+    dY, W = _as_f32(dY), _as_f32(W)
+    B, Co = dY.shape[:2]
+    Co2, C, r, _ = W.shape
+    if Co2 != Co or dY.shape[2] != H - r + 1 or dY.shape[3] != Wd - r + 1:
+        raise ValueError("shape mismatch")
+    dX = np.empty((B, C, H, Wd), dtype=np.float64)
+    rc = _load().oracle_conv_bwd_data_fp64(dY.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                           W.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                           dX.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B, C, Co, H, Wd, r)
+    if rc != 0:
+        raise ValueError("oracle_conv_bwd_data_fp64 rejected the shape")
+    return dX
+
+
+def conv_bwd_filter_fp64(I, dY, r: int) -> np.ndarray:
+    """dW[c'][c][p][q] = sum_{b,i,j} dY[b][c'][i][j] I[b][c][i+p][j+q] (the adjoint of Eq. 5 in W)
+    in fp64; I [B][C][H][W], dY [B][C'][H-r+1][W-r+1] float32 -> [C'][C][r][r]."""
+    I, dY = _as_f32(I), _as_f32(dY)
+    B, C, H, Wd = I.shape
+    Co = dY.shape[1]
+    if dY.shape[0] != B or dY.shape[2] != H - r + 1 or dY.shape[3] != Wd - r + 1:
+        raise ValueError("shape mismatch")
+    dW = np.empty((Co, C, r, r), dtype=np.float64)
+    rc = _load().oracle_conv_bwd_filter_fp64(I.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                             dY.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                             dW.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B, C, Co, H, Wd, r)
+    if rc != 0:
+        raise ValueError("oracle_conv_bwd_filter_fp64 rejected the shape")
+    return dW
 
 
 def num_threads() -> int:

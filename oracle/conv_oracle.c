@@ -147,6 +147,59 @@ int oracle_conv_nd_fp64(const float *I, const float *Wt, double *O, int nd, int 
     return 0;
 }
 
+/* Gradients of the same layer (the adjoints of Eq. 5, written out; not in the paper):
+ *   dX[b][c][y][x]    = sum_{c'} sum_{p,q : 0 <= y-p < Ho, 0 <= x-q < Wo} dY[b][c'][y-p][x-q] W[c'][c][p][q]
+ *   dW[c'][c][p][q]   = sum_b sum_{i<Ho} sum_{j<Wo} dY[b][c'][i][j] I[b][c][i+p][j+q]
+ * fp64 accumulation in (c', p, q) / (b, i, j) order; parallel over output planes only. */
+int oracle_conv_bwd_data_fp64(const float *dY, const float *Wt, double *dX, int B, int C, int Cout, int H, int W,
+                              int r)
+{
+    if (B < 1 || C < 1 || Cout < 1 || r < 1 || H < r || W < r) return -1;
+    const int Ho = H - r + 1, Wo = W - r + 1;
+    const long long planes = (long long)B * C;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long bc = 0; bc < planes; ++bc) {
+        const int b = (int)(bc / C), c = (int)(bc % C);
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                double acc = 0.0;
+                for (int co = 0; co < Cout; ++co)
+                    for (int p = 0; p < r; ++p)
+                        for (int q = 0; q < r; ++q) {
+                            const int i = y - p, j = x - q;
+                            if (i < 0 || i >= Ho || j < 0 || j >= Wo) continue;
+                            acc += (double)dY[(((size_t)b * Cout + co) * Ho + i) * Wo + j] *
+                                   (double)Wt[(((size_t)co * C + c) * r + p) * r + q];
+                        }
+                dX[(((size_t)b * C + c) * H + y) * W + x] = acc;
+            }
+    }
+    return 0;
+}
+
+int oracle_conv_bwd_filter_fp64(const float *I, const float *dY, double *dW, int B, int C, int Cout, int H, int W,
+                                int r)
+{
+    if (B < 1 || C < 1 || Cout < 1 || r < 1 || H < r || W < r) return -1;
+    const int Ho = H - r + 1, Wo = W - r + 1;
+    const long long planes = (long long)Cout * C;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (long long cc = 0; cc < planes; ++cc) {
+        const int co = (int)(cc / C), c = (int)(cc % C);
+        for (int p = 0; p < r; ++p)
+            for (int q = 0; q < r; ++q) {
+                double acc = 0.0;
+                for (int b = 0; b < B; ++b)
+                    for (int i = 0; i < Ho; ++i)
+                        for (int j = 0; j < Wo; ++j)
+                            acc += (double)dY[(((size_t)b * Cout + co) * Ho + i) * Wo + j] *
+                                   (double)I[(((size_t)b * C + c) * H + i + p) * W + j + q];
+                dW[(((size_t)co * C + c) * r + p) * r + q] = acc;
+            }
+    }
+    return 0;
+}
+
 /* Threads the OpenMP runtime will use (reported as cpu_baseline.cores). */
 int oracle_num_threads(void)
 {

@@ -144,6 +144,9 @@ def load(build_if_missing: bool = False):
         "conv_eshard_forward_b": ([vp, vp, vp, vp, vp, sz, vp], i),
         "conv_eshard_forward_c": ([vp, vp, vp, vp, sz, vp], i),
         "conv_eshard_destroy": ([vp], None),
+        "conv_plan_backward": ([ctypes.POINTER(vp)] + [i] * 9 + [ctypes.POINTER(PlanOptions)], i),
+        "conv_backward_data": ([vp, vp, vp, vp, vp, sz, vp], i),
+        "conv_backward_filter": ([vp, vp, vp, vp, vp, sz, vp], i),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)
@@ -362,6 +365,56 @@ class Plan:
         G = (ctypes.c_double * (t * r))()
         _check(load().conv_plan_winograd_matrices(self._h, AT, BT, G))
         return list(AT), list(BT), list(G)
+
+
+class BackwardPlan:
+    """conv_plan_backward: gradients of the layer through the fast forward pipeline
+    (which = "data": dX from dY and W; "filter": dW from X and dY)."""
+
+    def __init__(self, which: str, B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto", **opts):
+        lib = load()
+        h = ctypes.c_void_p()
+        o = options(gemm, **opts)
+        k = {"data": 1, "filter": 2}[which]
+        _check(lib.conv_plan_backward(ctypes.byref(h), k, B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o)))
+        self._h = h
+        self.which = which
+        self.workspace_bytes = int(lib.conv_workspace_bytes(h))
+        info = PlanInfo()
+        _check(lib.conv_plan_get_info(h, ctypes.byref(info)))
+        self.info = info.as_dict()
+        self.x_shape = (B, C, H, W)
+        self.w_shape = (Cout, C, r, r)
+        self.y_shape = (B, Cout, H - r + 1, W - r + 1)
+
+    def alloc_workspace(self, device=None) -> torch.Tensor:
+        return torch.empty(max(self.workspace_bytes, 16), dtype=torch.uint8, device=device or "cuda")
+
+    def data(self, dy, w, dx=None, workspace=None, stream=None) -> torch.Tensor:
+        _check_tensor(dy, "dy", self.y_shape)
+        _check_tensor(w, "weights", self.w_shape)
+        dx = torch.empty(self.x_shape, device=dy.device) if dx is None else dx
+        _check_tensor(dx, "dx", self.x_shape)
+        ws = self.alloc_workspace(dy.device) if workspace is None else workspace
+        _check(load().conv_backward_data(self._h, dy.data_ptr(), w.data_ptr(), dx.data_ptr(), ws.data_ptr(),
+                                         _nbytes(ws), _stream_ptr(stream)))
+        return dx
+
+    def filter(self, x, dy, dw=None, workspace=None, stream=None) -> torch.Tensor:
+        _check_tensor(x, "x", self.x_shape)
+        _check_tensor(dy, "dy", self.y_shape)
+        dw = torch.empty(self.w_shape, device=x.device) if dw is None else dw
+        _check_tensor(dw, "dw", self.w_shape)
+        ws = self.alloc_workspace(x.device) if workspace is None else workspace
+        _check(load().conv_backward_filter(self._h, x.data_ptr(), dy.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+                                           _nbytes(ws), _stream_ptr(stream)))
+        return dw
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_destroy(h)
+            self._h = None
 
 
 class EShard:

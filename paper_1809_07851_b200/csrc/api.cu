@@ -880,6 +880,7 @@ conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, in
 
 void conv_destroy(conv_plan_t p) {
     if (!p) return;
+    if (p->inner) conv_destroy(p->inner);
     if (p->d_consts || p->d_nd || p->h2d || p->d2h) {
         int cur = -1;
         cudaGetDevice(&cur);
@@ -1075,6 +1076,10 @@ static conv_status check_forward_args(conv_plan_s *p, const float *in, const flo
         fc_set_error("NULL plan");
         return CONV_ERR_INVALID_ARG;
     }
+    if (p->kind) {
+        fc_set_error("a backward plan runs through conv_backward_data / conv_backward_filter only");
+        return CONV_ERR_INVALID_ARG;
+    }
     conv_status st = check_device(p);
     if (st) return st;
     if ((st = check_dev_ptr(p, in, "in"))) return st;
@@ -1144,6 +1149,10 @@ conv_status conv_transform_weights(conv_plan_t p, const float *w, void *ws, size
         fc_set_error("NULL plan");
         return CONV_ERR_INVALID_ARG;
     }
+    if (p->kind) {
+        fc_set_error("a backward plan runs through conv_backward_data / conv_backward_filter only");
+        return CONV_ERR_INVALID_ARG;
+    }
     if (p->g.method == CONV_DIRECT) {
         fc_set_error("direct plans have no kernel transform");
         return CONV_ERR_UNSUPPORTED;
@@ -1163,6 +1172,10 @@ conv_status conv_forward_cached(conv_plan_t p, const float *in, float *out, void
                                 void *stream) {
     if (!p) {
         fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->kind) {
+        fc_set_error("a backward plan runs through conv_backward_data / conv_backward_filter only");
         return CONV_ERR_INVALID_ARG;
     }
     if (p->g.method == CONV_DIRECT) {
@@ -1185,6 +1198,10 @@ conv_status conv_run_stage(conv_plan_t p, int stage, const float *in, const floa
                            void *ws, size_t ws_bytes, void *stream) {
     if (!p) {
         fc_set_error("NULL plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (p->kind) {
+        fc_set_error("a backward plan runs through conv_backward_data / conv_backward_filter only");
         return CONV_ERR_INVALID_ARG;
     }
     if (p->g.method == CONV_DIRECT) {
@@ -1383,6 +1400,10 @@ conv_status conv_graph_create(conv_plan_t p, const float *in, const float *w, fl
     }
     *out_graph = nullptr;
     conv_status st;
+    if (p && p->kind) {
+        fc_set_error("a backward plan runs through conv_backward_data / conv_backward_filter only");
+        return CONV_ERR_INVALID_ARG;
+    }
     if (cached) {
         if (!p || p->g.method == CONV_DIRECT) {
             fc_set_error("cached graphs need a fast-method plan");
@@ -1811,6 +1832,127 @@ conv_status conv_eshard_forward_c(conv_eshard_t e, const void *x_recv, float *ou
         src += e->x_recv[j];
     }
     return run_stage(&e->lpx, g, 3, nullptr, nullptr, out, b, s);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Backward passes (not in the paper, which times forward layers).
+// Both gradients of Eq. 5 are themselves valid cross-correlations, so they run through the
+// same fast forward pipeline after a re-layout of their operands (backward.cu kernels):
+//   data    dX[b][c][y][x] = sum_{c'} sum_{p,q} dY[b][c'][y-p][x-q] W[c'][c][p][q]
+//           = forward( pad_{r-1}(dY) as [B][C'][H+r-1][W+r-1],  Wf[c][c'][p][q] =
+//             W[c'][c][r-1-p][r-1-q] ),  any method / tile of the forward plan
+//   filter  dW[c'][c][p][q] = sum_b sum_{i,j} dY[b][c'][i][j] X[b][c][i+p][j+q]
+//           = forward( X^T [C][B][H][W] (images <-> channels),  dY^T [C'][B][Ho][Wo] as an
+//             Ho x Wo (non-isotropic) kernel ) = [C][C'][r][r], transposed to [C'][C][r][r];
+//             FFT tiles of the whole image (t = H, W <= 64; conv_plan_nd) or the direct path
+// ---------------------------------------------------------------------------
+cudaError_t fc_launch_pad(const float *src, float *dst, long long planes, int h, int w, int pad, cudaStream_t s);
+cudaError_t fc_launch_flip_transpose(const float *w, float *wf, int Cout, int C, int r, cudaStream_t s);
+cudaError_t fc_launch_swap01(const float *src, float *dst, int A, int B, long long inner, cudaStream_t s);
+
+extern "C" {
+
+conv_status conv_plan_backward(conv_plan_t *out, int which, int B, int C, int Cout, int H, int W, int r,
+                               conv_method method, int m, const conv_plan_options *opts) {
+    if (!out || (which != 1 && which != 2)) {
+        fc_set_error("conv_plan_backward: NULL plan pointer or which not 1 (data) / 2 (filter)");
+        return CONV_ERR_INVALID_ARG;
+    }
+    if (B < 1 || C < 1 || Cout < 1 || r < 1 || H < r || W < r) {
+        fc_set_error("sizes must be >= 1 and H, W >= r");
+        return CONV_ERR_INVALID_ARG;
+    }
+    const int Ho = H - r + 1, Wo = W - r + 1;
+    conv_plan_t inner = nullptr;
+    conv_status st;
+    if (which == 1) {
+        st = plan_create(&inner, 0, B, Cout, C, H + r - 1, W + r - 1, r, method, m, nullptr, nullptr, nullptr, opts);
+    } else {
+        if (method == CONV_WINOGRAD) {
+            fc_set_error("backward filter: the Ho x Wo kernel exceeds Winograd's t <= 8; use an FFT or direct method");
+            return CONV_ERR_UNSUPPORTED;
+        }
+        const int in[2] = {H, W}, k[2] = {Ho, Wo}, mt[2] = {r, r};
+        st = plan_create(&inner, 2, C, B, Cout, 0, 0, 0, method, 0, in, k, mt, opts);
+    }
+    if (st) return st;
+    conv_plan_s *p = (conv_plan_s *)calloc(1, sizeof(conv_plan_s));
+    if (!p) {
+        conv_destroy(inner);
+        return CONV_ERR_OUT_OF_MEMORY;
+    }
+    p->kind = which;
+    p->inner = inner;
+    p->g = inner->g;
+    p->info = inner->info;
+    p->device = inner->device;
+    p->gemm = inner->gemm;
+    const size_t a = which == 1 ? (size_t)B * Cout * (H + r - 1) * (size_t)(W + r - 1) * 4   // padded dY
+                                : (size_t)B * C * (size_t)H * W * 4;                         // X^T
+    const size_t b = which == 1 ? (size_t)Cout * C * r * r * 4                                 // flipped W
+                                : (size_t)B * Cout * (size_t)Ho * Wo * 4;                     // dY^T
+    p->off_a = 0;
+    p->off_b = align256(a);
+    const size_t extra = align256(a) + align256(b) + (which == 2 ? align256((size_t)C * Cout * r * r * 4) : 0);
+    p->ws_bytes = extra + inner->ws_bytes;
+    p->info.workspace_bytes = p->ws_bytes;
+    *out = p;
+    return CONV_OK;
+}
+
+static conv_status backward_check(conv_plan_s *p, int which, void *ws, size_t ws_bytes) {
+    if (!p || p->kind != which) {
+        fc_set_error(which == 1 ? "not a backward-data plan" : "not a backward-filter plan");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_status st = check_device(p);
+    if (st) return st;
+    if (ws_bytes < p->ws_bytes) {
+        fc_set_error("workspace %zu bytes < required %zu", ws_bytes, p->ws_bytes);
+        return CONV_ERR_INVALID_ARG;
+    }
+    return check_dev_ptr(p, ws, "workspace");
+}
+
+conv_status conv_backward_data(conv_plan_t p, const float *dy, const float *w, float *dx, void *ws, size_t ws_bytes,
+                               void *stream) {
+    conv_status st = backward_check(p, 1, ws, ws_bytes);
+    if (st) return st;
+    if ((st = check_dev_ptr(p, dy, "dy")) || (st = check_dev_ptr(p, w, "weights")) || (st = check_dev_ptr(p, dx, "dx")))
+        return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geometry &g = p->inner->g;  // forward on (B, C', C, H + r - 1, W + r - 1, r)
+    char *b = (char *)ws;
+    float *dyp = (float *)(b + p->off_a), *wf = (float *)(b + p->off_b);
+    const int r = g.r;
+    if ((st = launch_result(fc_launch_pad(dy, dyp, (long long)g.B * g.C, g.H - 2 * (r - 1), g.W - 2 * (r - 1), r - 1, s),
+                            "pad dY")))
+        return st;
+    if ((st = launch_result(fc_launch_flip_transpose(w, wf, g.C, g.Cout, r, s), "flip / transpose W"))) return st;
+    const size_t extra = p->ws_bytes - p->inner->ws_bytes;
+    return forward_impl(p->inner, dyp, wf, dx, b + extra, s, nullptr);
+}
+
+conv_status conv_backward_filter(conv_plan_t p, const float *x, const float *dy, float *dw, void *ws,
+                                 size_t ws_bytes, void *stream) {
+    conv_status st = backward_check(p, 2, ws, ws_bytes);
+    if (st) return st;
+    if ((st = check_dev_ptr(p, x, "x")) || (st = check_dev_ptr(p, dy, "dy")) || (st = check_dev_ptr(p, dw, "dw")))
+        return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geometry &g = p->inner->g;  // forward on (B' = C, C' = B, Cout, H x W, kernel Ho x Wo)
+    char *b = (char *)ws;
+    float *xt = (float *)(b + p->off_a), *dyt = (float *)(b + p->off_b);
+    const int C = g.B, Bn = g.C, Cout = g.Cout;
+    const int H = g.ax_in[1], W = g.ax_in[2], Ho = g.ax_r[1], Wo = g.ax_r[2], r = H - Ho + 1;
+    if ((st = launch_result(fc_launch_swap01(x, xt, Bn, C, (long long)H * W, s), "X^T"))) return st;
+    if ((st = launch_result(fc_launch_swap01(dy, dyt, Bn, Cout, (long long)Ho * Wo, s), "dY^T"))) return st;
+    const size_t extra = p->ws_bytes - p->inner->ws_bytes;
+    float *dwt = (float *)(b + extra - align256((size_t)C * Cout * r * r * 4));  // [C][C'][r][r]
+    if ((st = forward_impl(p->inner, xt, dyt, dwt, b + extra, s, nullptr))) return st;
+    return launch_result(fc_launch_swap01(dwt, dw, C, Cout, (long long)r * r, s), "dW transpose");
 }
 
 }  // extern "C"

@@ -112,6 +112,9 @@ struct conv_plan_s {
     size_t off_V, off_Vlo, off_U, off_X, ws_bytes;
     size_t off_vscale, off_umax;          // F16X3: per-c' scales [2][Cout], per-image max|U| [B] (else 0)
     int chunk, nchunks;                   // L2-resident batch chunking (images per chunk)
+    int kind;                             // 0 forward; 1 / 2 backward data / filter (conv_plan_backward)
+    conv_plan_s *inner;                   // backward plans: the forward plan they run
+    size_t off_a, off_b;                  // backward plans: workspace offsets of the re-laid-out operands
     int e2e_chunks;                       // pipelining depth of conv_forward_host
     cudaStream_t h2d, d2h;                // copy streams of the pipelined host path
     conv_plan_info info;

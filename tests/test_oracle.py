@@ -227,3 +227,49 @@ def test_nd_rejects_bad_shapes():
         oracle.conv_nd_fp64(np.zeros((1, 2, 3, 3, 3, 3), np.float32), np.zeros((1, 2, 1, 1, 1, 1), np.float32))
     with pytest.raises(ValueError):
         oracle.conv_nd_fp64(np.zeros((1, 2, 3), np.float32), np.zeros((1, 2, 4), np.float32))
+
+
+# ----------------------------------------------------------- gradients ---
+# oracle.conv_bwd_data_fp64 / conv_bwd_filter_fp64 (the adjoints of Eq. 5, written out)
+
+def test_backward_adjoint_identities_exact():
+    """<conv(I, W), dY> = <I, bwd_data(dY, W)> = <W, bwd_filter(I, dY)>, exactly on integer data
+    (every fp64 sum exact): a transposed or shifted index in either gradient breaks it."""
+    I = _int_data((2, 3, 7, 8), 21, -3, 3)
+    W = _int_data((4, 3, 3, 3), 22, -3, 3)
+    dY = _int_data((2, 4, 5, 6), 23, -3, 3)
+    O = oracle.conv_fp64(I, W)
+    lhs = float(np.sum(O * dY))
+    dX = oracle.conv_bwd_data_fp64(dY, W, 7, 8)
+    dW = oracle.conv_bwd_filter_fp64(I, dY, 3)
+    assert lhs == float(np.sum(I.astype(np.float64) * dX)) == float(np.sum(W.astype(np.float64) * dW))
+
+
+def test_backward_against_torch_autograd_fp64():
+    """torch.nn.grad.conv2d_input / conv2d_weight in float64 on CPU (library routines)."""
+    g = torch.Generator().manual_seed(5)
+    I = torch.randn(2, 3, 9, 10, generator=g)
+    W = torch.randn(4, 3, 3, 3, generator=g)
+    dY = torch.randn(2, 4, 7, 8, generator=g)
+    dX = oracle.conv_bwd_data_fp64(dY, W, 9, 10)
+    dW = oracle.conv_bwd_filter_fp64(I, dY, 3)
+    rx = torch.nn.grad.conv2d_input(I.shape, W.double(), dY.double()).numpy()
+    rw = torch.nn.grad.conv2d_weight(I.double(), W.shape, dY.double()).numpy()
+    assert np.abs(dX - rx).max() <= 1e-12 * np.abs(rx).max()
+    assert np.abs(dW - rw).max() <= 1e-12 * np.abs(rw).max()
+
+
+def test_backward_delta_cases():
+    """A single-tap kernel moves dY back to the tap's offset (data); a single nonzero dY picks
+    the input patch under it (filter)."""
+    dY = _int_data((1, 1, 4, 5), 24)
+    W = np.zeros((1, 1, 3, 3), np.float32)
+    W[0, 0, 1, 2] = 1.0
+    dX = oracle.conv_bwd_data_fp64(dY, W, 6, 7)
+    ref = np.zeros((1, 1, 6, 7))
+    ref[0, 0, 1:5, 2:7] = dY[0, 0]
+    assert np.array_equal(dX, ref)
+    I = _int_data((1, 2, 6, 7), 25)
+    d = np.zeros((1, 1, 4, 5), np.float32)
+    d[0, 0, 2, 3] = 1.0
+    assert np.array_equal(oracle.conv_bwd_filter_fp64(I, d, 3)[0], I[0, :, 2:5, 3:6].astype(np.float64))
