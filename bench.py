@@ -495,7 +495,7 @@ def main():
     torch.cuda.synchronize()
     # per-launch CUDA events recorded by the library itself (conv_forward_timed): the
     # timed loop runs exactly the launches of conv_forward, with no host sync inside
-    timer = fc.StageTimer((plan.launches + 1) * args.steps + 8)  # + 1 start marker per call
+    timer = fc.StageTimer((plan.launches + 2) * args.steps + 8)  # + 2 start markers per call (NK1 || NK2)
 
     def on_step(k):
         if args.steps >= 200 and k == args.steps // 2:

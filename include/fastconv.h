@@ -103,6 +103,8 @@ typedef struct {
     int single_cta_mma;       /* 0 (default): CTA-pair contraction tiles when M > 128;
                                  1: single-CTA tiles */
     int e2e_chunks;           /* pipelining depth of conv_forward_host (0 = default 8) */
+    int overlap_kernel_transform;  /* -1 (default): NK1 runs on a plan-owned stream concurrently
+                                 with NK2 (they are independent; NK3 waits for both); 0: serial */
 } conv_plan_options;
 
 /* Fill `o` with the defaults (NULL-safe). */
@@ -277,7 +279,7 @@ int conv_forward_launch_count(conv_plan_t p);
 /* Per-stage timing without host synchronisation inside a timed loop:
  * conv_forward_timed() is conv_forward() plus a CUDA event recorded on `stream`
  * before the first and after every kernel launch (events pre-created by
- * conv_timer_create: one call consumes launch_count + 1 of the max_launches + 64).  conv_timer_read()
+ * conv_timer_create: one call consumes at most launch_count + 2 of the max_launches + 64: a start marker on each stream, NK1 running on the plan's auxiliary stream).  conv_timer_read()
  * synchronises on the last event and returns, per stage, the sum of the recorded
  * launch durations in ms (stage_ms[0..3] = NK1..NK4; the direct path reports in
  * [2]) and the number of launches recorded.  conv_timer_reset() rewinds. */

@@ -41,7 +41,7 @@ class PlanOptions(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int), ("gemm", ctypes.c_int), ("gauss_combine", ctypes.c_int),
                 ("complex_mode", ctypes.c_int), ("chunk_images", ctypes.c_int),
                 ("generic_transforms", ctypes.c_int), ("single_cta_mma", ctypes.c_int),
-                ("e2e_chunks", ctypes.c_int)]
+                ("e2e_chunks", ctypes.c_int), ("overlap_kernel_transform", ctypes.c_int)]
 
 
 def options(gemm: str = "auto", **kw) -> PlanOptions:

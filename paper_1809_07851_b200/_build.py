@@ -33,15 +33,17 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra_flags=(), out: str | None = None) -> str:
     """Compile every .cu to an object in parallel (one nvcc per translation unit), then
-    link the shared library."""
-    if not force and not _stale():
+    link the shared library.  extra_flags / out: experiment builds (A/B variants) into
+    another library path; the product library is LIB, built with no extra flags."""
+    target = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build") if out is None else target + ".objs"
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)] + list(extra_flags)
     jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
@@ -49,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         results = list(ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs))
     log = os.path.join(PKG, "build.log")
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp] + \
         [j[1] for j in jobs] + ["-lcuda"] * 0
     with open(log, "w") as f:
@@ -64,8 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("link failed (see %s):\n%s" % (log, res.stderr[-4000:]))
     if verbose:
         print("".join(r.stderr for r in results))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

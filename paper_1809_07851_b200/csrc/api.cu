@@ -247,7 +247,8 @@ static conv_status check_options(const conv_plan_options *o) {
     }
     if (o->gauss_combine < -1 || o->gauss_combine > 1 || o->complex_mode < -1 || o->complex_mode > 1 ||
         o->chunk_images < 0 || o->generic_transforms < 0 || o->generic_transforms > 1 || o->single_cta_mma < 0 ||
-        o->single_cta_mma > 1 || o->e2e_chunks < 0) {
+        o->single_cta_mma > 1 || o->e2e_chunks < 0 || o->overlap_kernel_transform < -1 ||
+        o->overlap_kernel_transform > 1) {
         fc_set_error("conv_plan_options field out of range");
         return CONV_ERR_INVALID_ARG;
     }
@@ -635,6 +636,7 @@ void conv_plan_options_init(conv_plan_options *o) {
     o->generic_transforms = 0;
     o->single_cta_mma = 0;
     o->e2e_chunks = 0;
+    o->overlap_kernel_transform = -1;
 }
 
 static const conv_plan_options *opts_or_default(const conv_plan_options *o, conv_plan_options *tmp) {
@@ -813,6 +815,11 @@ static conv_status plan_create(conv_plan_t *out, int nd, int B, int C, int Cout,
             if (e != cudaSuccess) {
                 fc_set_error("N-D constants: %s", cudaGetErrorString(e));
                 if (p->d_nd) cudaFree(p->d_nd);
+        if (p->aux) cudaStreamDestroy(p->aux);
+        for (int i = 0; i < FC_EVPAIRS; ++i) {
+            if (p->fork_ev[i]) cudaEventDestroy(p->fork_ev[i]);
+            if (p->join_ev[i]) cudaEventDestroy(p->join_ev[i]);
+        }
                 cudaFree(p->d_consts);
                 free(p);
                 return e == cudaErrorMemoryAllocation ? CONV_ERR_OUT_OF_MEMORY : CONV_ERR_CUDA;
@@ -834,6 +841,17 @@ static conv_status plan_create(conv_plan_t *out, int nd, int B, int C, int Cout,
     p->chunk = p->info.chunk;
     p->nchunks = p->info.nchunks;
     p->e2e_chunks = opts.e2e_chunks > 0 ? opts.e2e_chunks : 8;
+    p->overlap_nk1 = opts.overlap_kernel_transform != 0 && method != CONV_DIRECT;
+    if (p->overlap_nk1) {  // NK1 || NK2: an auxiliary stream and fork / join events
+        bool ok = cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking) == cudaSuccess;
+        for (int i = 0; ok && i < FC_EVPAIRS; ++i)
+            ok = cudaEventCreateWithFlags(&p->fork_ev[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&p->join_ev[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {  // fall back to the serial order
+            cudaGetLastError();
+            p->overlap_nk1 = 0;
+        }
+    }
     if (method != CONV_DIRECT && p->e2e_chunks > 1) {  // copy streams for the pipelined host path
         if (cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking) != cudaSuccess) {
@@ -881,12 +899,17 @@ conv_status conv_plan(conv_plan_t *out, int B, int C, int Cout, int H, int W, in
 void conv_destroy(conv_plan_t p) {
     if (!p) return;
     if (p->inner) conv_destroy(p->inner);
-    if (p->d_consts || p->d_nd || p->h2d || p->d2h) {
+    if (p->d_consts || p->d_nd || p->h2d || p->d2h || p->aux) {
         int cur = -1;
         cudaGetDevice(&cur);
         if (cur != p->device) cudaSetDevice(p->device);
         if (p->d_consts) cudaFree(p->d_consts);
         if (p->d_nd) cudaFree(p->d_nd);
+        if (p->aux) cudaStreamDestroy(p->aux);
+        for (int i = 0; i < FC_EVPAIRS; ++i) {
+            if (p->fork_ev[i]) cudaEventDestroy(p->fork_ev[i]);
+            if (p->join_ev[i]) cudaEventDestroy(p->join_ev[i]);
+        }
         if (p->h2d) cudaStreamDestroy(p->h2d);
         if (p->d2h) cudaStreamDestroy(p->d2h);
         if (cur >= 0 && cur != p->device) cudaSetDevice(cur);
@@ -1107,30 +1130,53 @@ struct conv_timer_s {
 // NK2 -> NK3 -> NK4 per chunk of images so U and X stay L2-resident.
 static conv_status forward_impl(conv_plan_s *p, const float *in, const float *w, float *out, char *ws,
                                 cudaStream_t s, conv_timer_s *t, bool skip_nk1 = false) {
-    auto mark = [&](int stage) -> conv_status {
+    auto mark_on = [&](int stage, cudaStream_t st_) -> conv_status {
         if (!t) return CONV_OK;
         if (t->used >= (int)t->ev.size()) {
             fc_set_error("conv_timer capacity exceeded");
             return CONV_ERR_INVALID_ARG;
         }
         t->stage[t->used] = stage;
-        return launch_result(cudaEventRecord(t->ev[t->used++], s), "cudaEventRecord");
+        return launch_result(cudaEventRecord(t->ev[t->used++], st_), "cudaEventRecord");
     };
-    conv_status st = mark(-1);
-    if (st) return st;
+    auto mark = [&](int stage) { return mark_on(stage, s); };
     const Geometry &g = p->g;
+    conv_status st;
     if (g.method == CONV_DIRECT) {
+        if ((st = mark(-1))) return st;
         st = launch_result(g.nd ? fc_launch_nd_direct(g, in, w, out, s) : fc_launch_direct(g, in, w, out, s),
                            "NK5 direct");
         return st ? st : mark(2);
     }
-    if (!skip_nk1 && ((st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0)))) return st;
+    // NK1 (V from the weights) and NK2 (U from the input) are independent: with overlap on,
+    // NK1 runs on the plan's auxiliary stream concurrently with NK2, and the first NK3 waits
+    // for both (fork / join events; captured as parallel branches inside CUDA graphs)
+    cudaEvent_t join = nullptr;
+    if (!skip_nk1) {
+        if (p->overlap_nk1) {
+            const unsigned k = __atomic_fetch_add(&p->evc, 1u, __ATOMIC_RELAXED) % FC_EVPAIRS;
+            join = p->join_ev[k];
+            if ((st = launch_result(cudaEventRecord(p->fork_ev[k], s), "fork")) ||
+                (st = launch_result(cudaStreamWaitEvent(p->aux, p->fork_ev[k], 0), "fork wait")) ||
+                (st = mark_on(-1, p->aux)) || (st = run_stage(p, g, 0, in, w, out, ws, p->aux)) ||
+                (st = mark_on(0, p->aux)) || (st = launch_result(cudaEventRecord(join, p->aux), "join")))
+                return st;
+        } else if ((st = mark(-1)) || (st = run_stage(p, g, 0, in, w, out, ws, s)) || (st = mark(0))) {
+            return st;
+        }
+    }
+    if ((st = mark(-1))) return st;
     for (int b0 = 0; b0 < g.B; b0 += p->chunk) {
         const Geometry gc = fc_chunk_geometry(g, g.B - b0 < p->chunk ? g.B - b0 : p->chunk);
         const float *in_c = in + (size_t)b0 * g.C * (size_t)g.vin;
         float *out_c = out + (size_t)b0 * g.Cout * (size_t)g.vout;
-        for (int k = 1; k < 4; ++k)
+        for (int k = 1; k < 4; ++k) {
+            if (k == 2 && join) {
+                if ((st = launch_result(cudaStreamWaitEvent(s, join, 0), "join wait"))) return st;
+                join = nullptr;
+            }
             if ((st = run_stage(p, gc, k, in_c, w, out_c, ws, s)) || (st = mark(k))) return st;
+        }
     }
     return CONV_OK;
 }

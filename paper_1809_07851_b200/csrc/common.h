@@ -117,6 +117,13 @@ struct conv_plan_s {
     size_t off_a, off_b;                  // backward plans: workspace offsets of the re-laid-out operands
     int e2e_chunks;                       // pipelining depth of conv_forward_host
     cudaStream_t h2d, d2h;                // copy streams of the pipelined host path
+    // NK1 runs on `aux` concurrently with NK2 (they are independent; NK3 joins both):
+    // fork / join event pairs taken round-robin per forward call (thread-safe counter)
+    cudaStream_t aux;
+#define FC_EVPAIRS 32
+    cudaEvent_t fork_ev[FC_EVPAIRS], join_ev[FC_EVPAIRS];
+    unsigned evc;
+    int overlap_nk1;
     conv_plan_info info;
 };
 

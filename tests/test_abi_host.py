@@ -194,7 +194,7 @@ def test_library_reads_no_environment():
 def test_plan_options_validation(lib):
     o = fc.options()
     assert (o.gemm, o.gauss_combine, o.complex_mode, o.chunk_images, o.generic_transforms, o.single_cta_mma,
-            o.e2e_chunks) == (0, -1, -1, 0, 0, 0, 0)
+            o.e2e_chunks, o.overlap_kernel_transform) == (0, -1, -1, 0, 0, 0, 0, -1)
     info = fc.PlanInfo()
     bad = fc.options(gauss_combine=2)
     assert lib.conv_plan_query_opts(1, 4, 4, 16, 16, 3, 1, 4, ctypes.byref(bad), ctypes.byref(info)) == 1

@@ -30,7 +30,11 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print per-stage ms (best of --iters profiled runs)")
     ap.add_argument("--opt", action="append", default=[], help="plan option name=value (conv_plan_options)")
+    ap.add_argument("--lib", default=None, help="experiment build of the library (A/B variants)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_1809_07851_b200 import _build
+        _build.LIB = os.path.abspath(args.lib)
     cfg = synth.CONFIGS[args.config]
     if args.B:
         cfg = cfg.with_batch(args.B)
