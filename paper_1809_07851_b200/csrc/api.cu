@@ -266,12 +266,39 @@ static conv_status check_options(const conv_plan_options *o) {
 // section 7), and the contraction's tensor work counts the padded columns it really issues.
 // ---------------------------------------------------------------------------
 namespace {
+// Fraction of each stage's roofline the B200 kernels reach, measured over BASELINE.json's
+// configs with L2 flushed between steps (profiles/r02_autotune_flushed_configs.json):
+// the Winograd transforms 0.8-0.9; the FFT transforms depend on the tile edge t (codelet
+// radices, and the per-tile state -- t complex values per thread, m x h staged spectra per
+// tile -- that bounds the resident warps for large t); NK1 ~0.45;
+// NK3 ~0.85 of max(tensor, HBM).
 struct ModelEff {
     double nk1, nk2, nk3, nk4;
 };
-// Winograd / FFT transform families (measured fraction of the stage roofline, B200)
-constexpr ModelEff kEffWino = {0.50, 0.88, 0.88, 0.86};
-constexpr ModelEff kEffFft = {0.50, 0.75, 0.85, 0.70};
+ModelEff model_eff(int method, int t) {
+    // NK2 / NK4 per tile edge t (mean of VGG-1.2 and VGG-3.2, r02 flushed sweep)
+    struct TE {
+        int t;
+        double nk2, nk4;
+    };
+    static const TE wino[] = {{4, 0.81, 0.78}, {5, 0.78, 0.85}, {6, 0.93, 0.92}, {8, 0.84, 0.78}};
+    static const TE fft[] = {{4, 0.55, 0.42},  {5, 0.58, 0.45},  {6, 0.62, 0.55},  {7, 0.60, 0.50},
+                             {8, 0.70, 0.62},  {9, 0.70, 0.58},  {10, 0.68, 0.58}, {12, 0.72, 0.59},
+                             {13, 0.62, 0.56}, {14, 0.74, 0.57}, {15, 0.65, 0.53}, {16, 0.80, 0.67},
+                             {18, 0.60, 0.52}, {20, 0.63, 0.52}, {21, 0.53, 0.37}, {24, 0.58, 0.47},
+                             {25, 0.48, 0.41}, {27, 0.50, 0.43}, {28, 0.55, 0.35}, {30, 0.50, 0.42},
+                             {31, 0.30, 0.33}, {32, 0.42, 0.39}};
+    const bool w = method == CONV_WINOGRAD;
+    const TE *tab = w ? wino : fft;
+    const int n = w ? 4 : 22;
+    ModelEff e = {w ? 0.50 : 0.45, w ? 0.85 : 0.55, 0.85, w ? 0.85 : 0.45};
+    for (int i = 0; i < n; ++i)
+        if (tab[i].t == t) {
+            e.nk2 = tab[i].nk2;
+            e.nk4 = tab[i].nk4;
+        }
+    return e;
+}
 }  // namespace
 
 double fc_model_ms(const conv_plan_info &I, const Geometry &G) {
@@ -279,7 +306,7 @@ double fc_model_ms(const conv_plan_info &I, const Geometry &G) {
     const int gemm = I.gemm;
     const double peak = gemm == CONV_GEMM_TCGEN05_F16X3 ? 1634.2e12 / 3.0
                         : gemm == CONV_GEMM_TCGEN05_3XTF32 ? 0.5 * 1634.2e12 / 3.0 : 74.4e12;
-    const ModelEff &ef = G.method == CONV_WINOGRAD ? kEffWino : kEffFft;
+    const ModelEff ef = model_eff(G.method, G.t);
     const double eff[4] = {ef.nk1, ef.nk2, ef.nk3, ef.nk4};
     double t = 0.0;
     for (int s = 0; s < 4; ++s) {

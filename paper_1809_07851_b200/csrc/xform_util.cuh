@@ -51,9 +51,12 @@ __device__ __forceinline__ void store_strip(float *__restrict__ dst, const float
         for (int i = threadIdx.x; i < rows * Wo; i += blockDim.x) __stcs(dst + i, src[i]);
         return;
     }
-    if (Wo < 48) {  // narrow rows: flat index (one division per element) keeps every lane busy
+    if (Wo < 48) {  // narrow rows: flat index keeps every lane busy; the row from a float
+        // reciprocal (fc_sdiv, 3 instructions; the integer division it replaces made the deep
+        // layer's Winograd NK4 instruction-bound, ncu r02i)
+        const float inv = 1.f / (float)Wo;
         for (int idx = threadIdx.x; idx < rows * Wo; idx += blockDim.x) {
-            const int r = idx / Wo, c = idx - r * Wo;
+            const int r = fc_sdiv(idx, inv), c = idx - r * Wo;
             __stcs(dst + idx, src[r * SWo + c]);
         }
         return;
