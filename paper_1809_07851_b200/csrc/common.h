@@ -178,12 +178,13 @@ __device__ __forceinline__ void fc_store_v(float *V, float *Vlo, size_t o, float
         const __half hi = __float2half_rn(x);
         reinterpret_cast<__half *>(V)[o] = hi;
         reinterpret_cast<__half *>(Vlo)[o] = __float2half_rn(x - __half2float(hi));
-    } else if (split) {
+    } else if (split) {  // V_lo rounded to the nearest TF32 too (the MMA would truncate it)
         uint32_t r;
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
         const float hi = __uint_as_float(r);
         V[o] = hi;
-        Vlo[o] = v - hi;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v - hi));
+        Vlo[o] = __uint_as_float(r);
     } else {
         V[o] = v;
     }

@@ -38,6 +38,12 @@
 
 namespace {
 
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
 constexpr int NUM_THREADS = 384;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -406,11 +412,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < Cfg::B_BYTES / 16 / 128; ++j) {
                     const float4 v = bh[st + 128 * j];
+                    // U_hi = trunc_tf32(U) is what the MMA reads from the staged U; U_lo = U - U_hi
+                    // is exact in fp32 and rounded to the nearest TF32 here (the MMA would
+                    // truncate it: 2^-21 instead of 2^-22 relative to |U|)
                     float4 lo;
-                    lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                    lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                    lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                    lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    lo.x = rna_tf32(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u));
+                    lo.y = rna_tf32(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
+                    lo.z = rna_tf32(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u));
+                    lo.w = rna_tf32(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
                     bl[st + 128 * j] = lo;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
