@@ -879,14 +879,7 @@ static conv_status plan_create(conv_plan_t *out, int nd, int B, int C, int Cout,
             p->overlap_nk1 = 0;
         }
     }
-    if (method != CONV_DIRECT && p->e2e_chunks > 1) {  // copy streams for the pipelined host path
-        if (cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking) != cudaSuccess) {
-            cudaGetLastError();
-            if (p->h2d) cudaStreamDestroy(p->h2d);
-            p->h2d = p->d2h = nullptr;  // falls back to the serial host path
-        }
-    }
+    // the pipelined host path's copy streams are created on its first call (conv_forward_host)
     *out = p;
     return CONV_OK;
 }
@@ -1390,6 +1383,21 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
     const size_t nw = (size_t)g.Cout * g.C * (size_t)g.kvol * 4;
     cudaError_t e = cudaMemcpyAsync(d_w, h_w, nw, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return launch_result(e, "H2D copy (weights)");
+    if (g.method != CONV_DIRECT && p->e2e_chunks > 1 && !p->h2d) {  // first host call: copy streams
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!p->h2d) {
+            cudaStream_t a = nullptr, b = nullptr;
+            if (cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking) == cudaSuccess) {
+                p->d2h = b;
+                __atomic_store_n(&p->h2d, a, __ATOMIC_RELEASE);
+            } else {  // falls back to the serial host path
+                cudaGetLastError();
+                if (a) cudaStreamDestroy(a);
+            }
+        }
+    }
     if (g.method == CONV_DIRECT || !p->h2d || !p->d2h) {
         e = cudaMemcpyAsync(d_in, h_in, img_in * g.B * 4, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return launch_result(e, "H2D copy");

@@ -45,6 +45,12 @@ __device__ __forceinline__ float rna_tf32(float x) {
 }
 
 constexpr int NUM_THREADS = 384;
+// F16X3 kernel: warps 0-7 as the tf32 kernel's, then F16_SPLIT_WARPS splitter warps
+#ifndef FC_F16_SPLIT_WARPS
+#define FC_F16_SPLIT_WARPS 4
+#endif
+constexpr int F16_SPLIT_WARPS = FC_F16_SPLIT_WARPS;
+constexpr int F16_THREADS = 256 + 32 * F16_SPLIT_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -486,7 +492,7 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // SU stages ahead of the tensor cores instead of waiting for MMA completion.
 // Warp 0 lane 0 streams U, warp 2 lane 0 streams V (independent run-ahead).
 template <int CG, int BLOCK_N, int SA, int SU, bool GC>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(F16_THREADS, 1)
     nk3_gemm_tcgen05_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                          const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, int M,
                          int K, long long NP, int Z, int cplx, int Mh, int kb_half, int Cout,
@@ -525,12 +531,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < SA; ++s) {
             mbar_init(fullA_bar(s), 1);
-            mbar_init(split_bar(s), 4 * CG);
+            mbar_init(split_bar(s), F16_SPLIT_WARPS * CG);
             mbar_init(emptyA_bar(s), 1);
         }
         for (int s = 0; s < SU; ++s) {
             mbar_init(fullU_bar(s), 1);
-            mbar_init(emptyU_bar(s), 4);
+            mbar_init(emptyU_bar(s), F16_SPLIT_WARPS);
         }
         for (int a = 0; a < NACC; ++a) {
             mbar_init(tfull_bar(a), 1);
@@ -799,7 +805,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (warp >= 8) {
         // ---- splitter: fp32 U [BK][NH] -> scaled fp16 (hi, lo), K-major 64 B-swizzled rows
         const int st = threadIdx.x - 256;
-        static_assert(128 % Cfg::NH == 0, "a splitter thread converts one tile column n = st % NH");
+        constexpr int NSPL = 32 * F16_SPLIT_WARPS;
+        static_assert(NSPL % Cfg::NH == 0, "a splitter thread converts one tile column n = st % NH");
         const int ncol = st % Cfg::NH;
         int sa = 0, su = 0;
         uint32_t pa = 0, pu = 0;
@@ -815,8 +822,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 uint8_t *bh = gbase + sa * Cfg::A_STAGE + 2 * Cfg::A_BYTES;
                 uint8_t *bl = bh + Cfg::B_BYTES;
 #pragma unroll
-                for (int i = 0; i < Cfg::NH * BK / 8 / 128; ++i) {
-                    const int chunk = st + 128 * i;
+                for (int i = 0; i < Cfg::NH * BK / 8 / NSPL; ++i) {
+                    const int chunk = st + NSPL * i;
                     const int n = ncol, kg = chunk / Cfg::NH;  // 8 K values kg*8.. of column n
                     float x[8];
 #pragma unroll
@@ -987,7 +994,7 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
     const long long groups = tiles < g_num_sms / CG ? tiles : g_num_sms / CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(CG * groups));
-    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.blockDim = dim3(F16_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
