@@ -175,6 +175,11 @@ conv_status conv_plan_query_opts(int B, int C, int Cout, int H, int W, int r,
 conv_status conv_plan_best_m(int B, int C, int Cout, int H, int W, int r, conv_method method,
                              const conv_plan_options *opts, int *m_out, double *model_ms,
                              int max_cand, int *n_cand, int *cand_m, double *cand_ms);
+/* The paper's comparison rule across methods (each method at its best m, the fastest
+ * wins) on the same model: *method_out / *m_out get the predicted-fastest fast method and its
+ * tile, *model_ms (may be NULL) its predicted time.  Errors as conv_plan_best_m. */
+conv_status conv_plan_best_method(int B, int C, int Cout, int H, int W, int r, const conv_plan_options *opts,
+                                  conv_method *method_out, int *m_out, double *model_ms);
 
 /* Create a plan on the current CUDA device, which must be sm_100 (B200; the library
  * carries sm_100a code only -- other devices get CONV_ERR_UNSUPPORTED) (uploads ~KB of constants:

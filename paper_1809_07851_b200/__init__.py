@@ -105,6 +105,8 @@ def load(build_if_missing: bool = False):
         "conv_plan_options_init": ([ctypes.POINTER(PlanOptions)], None),
         "conv_plan_best_m": ([i] * 7 + [ctypes.POINTER(PlanOptions), ctypes.POINTER(i), dp, i,
                                         ctypes.POINTER(i), ctypes.POINTER(i), dp], i),
+        "conv_plan_best_method": ([i] * 6 + [ctypes.POINTER(PlanOptions), ctypes.POINTER(i), ctypes.POINTER(i),
+                                          dp], i),
         "conv_plan": ([ctypes.POINTER(vp)] + [i] * 8, i),
         "conv_plan_ex": ([ctypes.POINTER(vp)] + [i] * 9, i),
         "conv_plan_opts": ([ctypes.POINTER(vp)] + [i] * 8 + [ctypes.POINTER(PlanOptions)], i),
@@ -175,6 +177,16 @@ def plan_query(B, C, Cout, H, W, r, method: str, m: int = 0, gemm: str = "auto",
     o = options(gemm, **opts)
     _check(load().conv_plan_query_opts(B, C, Cout, H, W, r, METHODS[method], m, ctypes.byref(o), ctypes.byref(info)))
     return info.as_dict()
+
+
+def best_method(B, C, Cout, H, W, r, gemm: str = "auto", **opts):
+    """conv_plan_best_method: (method name, m, predicted ms) -- the paper's rule on
+    the calibrated stage-sum model."""
+    o = options(gemm, **opts)
+    meth, m, ms = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check(load().conv_plan_best_method(B, C, Cout, H, W, r, ctypes.byref(o), ctypes.byref(meth), ctypes.byref(m),
+                                        ctypes.byref(ms)))
+    return {v: k for k, v in METHODS.items()}[meth.value], m.value, ms.value
 
 
 def plan_query_nd(B, C, Cout, in_shape, kernel_shape, method: str, m=None, gemm: str = "auto", **opts) -> dict:
@@ -526,11 +538,14 @@ _PLAN_CACHE_MAX = 32
 def forward(x: torch.Tensor, w: torch.Tensor, method: str = "winograd", m: int = 4,
             gemm: str = "auto") -> torch.Tensor:
     """One-shot forward: plans (cached by shape, method, m, gemm and device), allocates the
-    workspace and output with torch, runs on the current stream.  m = 0: the planner's tile."""
+    workspace and output with torch, runs on the current stream.  m = 0: the planner's tile;
+    method = "auto": the planner's method and tile (conv_plan_best_method)."""
     B, C, H, W = x.shape
     Cout, C2, r, _ = w.shape
     if C2 != C:
         raise ValueError("channel mismatch")
+    if method == "auto":
+        method, m, _ = best_method(B, C, Cout, H, W, r, gemm)
     key = (B, C, Cout, H, W, r, method, m, gemm, x.device.index if x.is_cuda else -1)
     plan = _PLAN_CACHE.get(key)
     if plan is None:

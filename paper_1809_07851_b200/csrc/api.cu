@@ -684,6 +684,40 @@ conv_status conv_plan_query(int B, int C, int Cout, int H, int W, int r, conv_me
     return conv_plan_query_opts(B, C, Cout, H, W, r, method, m, nullptr, info);
 }
 
+conv_status conv_plan_best_method(int B, int C, int Cout, int H, int W, int r, const conv_plan_options *opts,
+                                  conv_method *method_out, int *m_out, double *model_ms) {
+    if (!method_out || !m_out) {
+        fc_set_error("conv_plan_best_method: NULL output");
+        return CONV_ERR_INVALID_ARG;
+    }
+    conv_plan_options d;
+    const conv_plan_options *o = opts_or_default(opts, &d);
+    int best_m = 0;
+    double best = 0.0;
+    conv_method best_meth = CONV_DIRECT;
+    conv_status last = CONV_ERR_UNSUPPORTED;
+    const conv_method order[3] = {CONV_WINOGRAD, CONV_REGULAR_FFT, CONV_GAUSS_FFT};
+    for (conv_method meth : order) {
+        int m = 0;
+        double ms = 0.0;
+        conv_status st = fc_best_m(B, C, Cout, H, W, r, (int)meth, o, &m, &ms, 0, nullptr, nullptr, nullptr);
+        if (st != CONV_OK) {
+            last = st;
+            continue;
+        }
+        if (!best_m || ms < best) {  // the paper's rule: each method at its best m, the fastest wins
+            best_m = m;
+            best = ms;
+            best_meth = meth;
+        }
+    }
+    if (!best_m) return last;
+    *method_out = best_meth;
+    *m_out = best_m;
+    if (model_ms) *model_ms = best;
+    return CONV_OK;
+}
+
 conv_status conv_plan_best_m(int B, int C, int Cout, int H, int W, int r, conv_method method,
                              const conv_plan_options *opts, int *m_out, double *model_ms, int max_cand, int *n_cand,
                              int *cand_m, double *cand_ms) {

@@ -258,3 +258,12 @@ def test_plan_query_nd_geometry(lib):
         fc.plan_query_nd(B, C, Co, (10, 12, 14), (3, 3, 3), "winograd", (2, 2, 7))  # t = 9 > 8
     with pytest.raises(fc.ConvError):
         fc.plan_query_nd(B, C, Co, (2, 12, 14), (3, 3, 3), "regular_fft", (2, 2, 2))  # input < kernel
+
+
+def test_best_method(lib):
+    """conv_plan_best_method: the fastest method at its best m on the calibrated model -- the
+    measured-best family on B200 for the BASELINE layers (profiles/r02j_flushed_configs.json)."""
+    assert fc.best_method(64, 256, 256, 58, 58, 3)[:2] == ("winograd", 4)      # VGG-3.2
+    assert fc.best_method(64, 64, 64, 226, 226, 3)[:2] == ("regular_fft", 14)  # VGG-1.2
+    assert fc.best_method(128, 96, 256, 31, 31, 5)[0].endswith("fft")         # 5x5
+    assert fc.best_method(64, 512, 512, 16, 16, 3)[:2] == ("winograd", 4)      # deep
