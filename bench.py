@@ -360,6 +360,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fastconv", choices=["fastconv", "reference"])
     ap.add_argument("--workload", default="vgg3_2")
+    ap.add_argument("--seed", type=int, default=None, help="override the config's input seed (synth)")
     ap.add_argument("--method", default="auto", help="auto (sweep) or winograd|regular_fft|gauss_fft|direct")
     ap.add_argument("--m", "--tile", dest="m", type=int, default=0)
     ap.add_argument("--gemm", default="auto", choices=["auto", "tcgen05", "ffma", "f16x3"])
@@ -414,7 +415,7 @@ def main():
 
     # one global seeded draw; rank k slices its images (strong: B/N each, weak: B each)
     gcfg = base if args.scaling == "strong" else base.with_batch(base.B * world)
-    I_all, W = synth.make_inputs(gcfg)
+    I_all, W = synth.make_inputs(gcfg, seed=args.seed)
     lo, hi = parallel.shard_range(gcfg.B, rank, world)
     I = I_all[lo:hi].contiguous()
     del I_all
