@@ -817,7 +817,10 @@ __global__ void __launch_bounds__(F16_THREADS, 1)
         for (int p = 0; p < SUB; ++p) {
             for (int kb = 0; kb < num_k; ++kb) {
                 mbar_wait(fullU_bar(su), pu);
-                mbar_wait(fullA_bar(sa), pa);  // V landed => the operand slot is free (producer waited)
+                // the operand slot is free once the MMAs that read it committed (the V producer waits
+                // on the same phase); converting does not wait for this stage's V to land -- only
+                // the arrival below does, so the conversion overlaps the V load
+                mbar_wait(emptyA_bar(sa), pa ^ 1);
                 const float *uf = reinterpret_cast<const float *>(gbase + (ubase - base) + su * Cfg::UF_BYTES);
                 uint8_t *bh = gbase + sa * Cfg::A_STAGE + 2 * Cfg::A_BYTES;
                 uint8_t *bl = bh + Cfg::B_BYTES;
@@ -843,6 +846,7 @@ __global__ void __launch_bounds__(F16_THREADS, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if ((st & 31) == 0) {
+                    mbar_wait(fullA_bar(sa), pa);  // this CTA's V landed: the split arrival carries it
                     I::arrive_leader(split_bar(sa));
                     Tc<1>::arrive_leader(emptyU_bar(su));  // local: the staging slot may be refilled
                 }
