@@ -1443,7 +1443,16 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
     // chunk i (caller's stream) and the D2H of chunk i-1 (second copy stream) overlap;
     // PCIe runs both directions at once.  The plan's own chunk (<= this one) sizes U / X.
     const int nck = p->e2e_chunks < g.B ? p->e2e_chunks : g.B;
-    const int per = (g.B + nck - 1) / nck;
+    // chunk boundaries: half-size first and last chunks (the first H2D and the last D2H are the
+    // pipeline's exposed ends), the rest split evenly
+    std::vector<int> bnd(1, 0);
+    {
+        const int edge = nck >= 3 ? std::max(1, g.B / (2 * nck)) : 0;
+        const int mid = g.B - 2 * edge, nm = nck >= 3 ? nck - 2 : nck;
+        if (edge) bnd.push_back(edge);
+        for (int k = 1; k <= nm; ++k) bnd.push_back(edge + (int)((long long)mid * k / nm));
+        if (edge) bnd.push_back(g.B);
+    }
     std::vector<cudaEvent_t> evs;
     auto mk = [&]() -> cudaEvent_t {
         cudaEvent_t ev = nullptr;
@@ -1458,8 +1467,9 @@ conv_status conv_forward_host(conv_plan_t p, const float *h_in, const float *h_w
         for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
         return st;
     }
-    for (int b0 = 0; b0 < g.B && e == cudaSuccess && !st; b0 += per) {
-        const int nb = g.B - b0 < per ? g.B - b0 : per;
+    for (size_t ci = 0; ci + 1 < bnd.size() && e == cudaSuccess && !st; ++ci) {
+        const int b0 = bnd[ci], nb = bnd[ci + 1] - bnd[ci];
+        if (nb <= 0) continue;
         cudaEvent_t in_ready = mk(), out_ready = mk();
         if (!in_ready || !out_ready) {
             e = cudaErrorMemoryAllocation;
