@@ -105,6 +105,14 @@ typedef struct {
     int e2e_chunks;           /* pipelining depth of conv_forward_host (0 = default 8) */
     int overlap_kernel_transform;  /* -1 (default): NK1 runs on a plan-owned stream concurrently
                                  with NK2 (they are independent; NK3 waits for both); 0: serial */
+    int fused;                /* Winograd F(2,3) (m = 2, r = 3, 2-D) with the 3xTF32 contraction:
+                                 NK2, NK3 and NK4 in ONE tcgen05 kernel -- the input transform in
+                                 the contraction's producer, the inverse transform in its epilogue,
+                                 U and X never leave the SM (PAPER.md P:455-460,
+                                 P:483-486 stream them through memory).  0 (default): staged
+                                 kernels; 1: fused (CONV_ERR_UNSUPPORTED unless eligible; gemm
+                                 AUTO then resolves to CONV_GEMM_TCGEN05_3XTF32, chunk_images 0).
+                                 Pays for small C' (the input transform is recomputed C'/32 times) */
 } conv_plan_options;
 
 /* Fill `o` with the defaults (NULL-safe). */
@@ -148,6 +156,9 @@ typedef struct {
                            3 Gauss-FFT (T1, T2, T3), or 2 when the F16X3 contraction combines
                            Gauss in its epilogue (Re = T1 - T3, Im = T1 + T2; C' % 32 == 0;
                            X is then [E][2C'][BN_pad] like Regular-FFT's); 0 for CONV_DIRECT */
+    int fused;          /* 1: NK2-NK4 run as one fused kernel (conv_plan_options.fused; no U / X
+                           in the workspace, alg_bytes[1] = alg_bytes[3] = 0 and alg_bytes[2] the
+                           fused kernel's input + V + output) */
 } conv_plan_info;
 
 /* Host-only: validate arguments and fill `info` (no CUDA calls).  m = 0 for a

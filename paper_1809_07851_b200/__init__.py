@@ -41,7 +41,8 @@ class PlanOptions(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int), ("gemm", ctypes.c_int), ("gauss_combine", ctypes.c_int),
                 ("complex_mode", ctypes.c_int), ("chunk_images", ctypes.c_int),
                 ("generic_transforms", ctypes.c_int), ("single_cta_mma", ctypes.c_int),
-                ("e2e_chunks", ctypes.c_int), ("overlap_kernel_transform", ctypes.c_int)]
+                ("e2e_chunks", ctypes.c_int), ("overlap_kernel_transform", ctypes.c_int),
+                ("fused", ctypes.c_int)]
 
 
 def options(gemm: str = "auto", **kw) -> PlanOptions:
@@ -68,7 +69,7 @@ class PlanInfo(ctypes.Structure):
                  ("gemm", ctypes.c_int), ("nd", ctypes.c_int)] +
                 [(n, ctypes.c_int * 3) for n in ("in_shape", "kernel_shape", "m_shape", "t_shape", "tiles",
                                                  "out_shape")] +
-                [("x_planes", ctypes.c_int)])
+                [("x_planes", ctypes.c_int), ("fused", ctypes.c_int)])
 
     def as_dict(self) -> dict:
         d = {}

@@ -248,7 +248,7 @@ static conv_status check_options(const conv_plan_options *o) {
     if (o->gauss_combine < -1 || o->gauss_combine > 1 || o->complex_mode < -1 || o->complex_mode > 1 ||
         o->chunk_images < 0 || o->generic_transforms < 0 || o->generic_transforms > 1 || o->single_cta_mma < 0 ||
         o->single_cta_mma > 1 || o->e2e_chunks < 0 || o->overlap_kernel_transform < -1 ||
-        o->overlap_kernel_transform > 1) {
+        o->overlap_kernel_transform > 1 || o->fused < 0 || o->fused > 1) {
         fc_set_error("conv_plan_options field out of range");
         return CONV_ERR_INVALID_ARG;
     }
@@ -386,7 +386,15 @@ static conv_status finish_geometry(Geometry &G, conv_plan_info *info, const conv
         } else {
             G.Z = G.E; G.M = Cout; G.K = C;
         }
-        G.vf16 = gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO;  // AUTO: query-time default
+        G.fused = opts->fused == 1;
+        if (G.fused && (method != CONV_WINOGRAD || G.m != 2 || G.r != 3 || G.nd != 0 || opts->chunk_images != 0 ||
+                        (gemm != CONV_GEMM_AUTO && gemm != CONV_GEMM_TCGEN05_3XTF32))) {
+            fc_set_error("fused NK2-NK4 needs 2-D Winograd F(2,3), the 3xTF32 contraction (gemm AUTO or "
+                         "TCGEN05_3XTF32) and chunk_images 0");
+            return CONV_ERR_UNSUPPORTED;
+        }
+        // AUTO: query-time default F16X3 (fused plans: 3xTF32)
+        G.vf16 = !G.fused && (gemm == CONV_GEMM_TCGEN05_F16X3 || gemm == CONV_GEMM_AUTO);
         const int kq = G.vf16 ? 8 : 4;  // V row pitch: 16 bytes of fp16 / fp32
         G.Kp = (G.K + kq - 1) / kq * kq;
         G.gc = method == CONV_GAUSS_FFT && G.vf16 && Cout % 32 == 0 && gauss_combine_pays(G, opts->gauss_combine);
@@ -418,7 +426,8 @@ static conv_status finish_geometry(Geometry &G, conv_plan_info *info, const conv
     I.direct_flops = 2.0 * B * (double)C * Cout * vout * kv;
     I.chunk = B;
     I.nchunks = 1;
-    I.gemm = gemm == CONV_GEMM_AUTO ? CONV_GEMM_TCGEN05_F16X3 : gemm;
+    I.gemm = gemm == CONV_GEMM_AUTO ? (G.fused ? CONV_GEMM_TCGEN05_3XTF32 : CONV_GEMM_TCGEN05_F16X3) : gemm;
+    I.fused = G.fused;
     I.x_planes = method == CONV_DIRECT ? 0 : (G.gc ? 2 : G.planes);
     if (method != CONV_DIRECT) {
         const int split = (gemm != CONV_GEMM_FFMA);
@@ -447,6 +456,13 @@ static conv_status finish_geometry(Geometry &G, conv_plan_info *info, const conv
         // element-wise FLOPs: 2t^2 BNCC' / 8 t h BNCC' / 6 t h BNCC'
         const double k = method == CONV_WINOGRAD ? 2.0 : (method == CONV_REGULAR_FFT ? 8.0 : 6.0);
         I.alg_flops[2] = k * G.E * BN * CCp;
+        if (G.fused) {  // one kernel: input + V (hi, lo) + output; no U / X in the workspace
+            I.bytes_U = I.bytes_X = 0;
+            I.workspace_bytes = align256(I.bytes_V);
+            I.alg_bytes[2] = 4.0 * B * C * vin + 4.0 * wEr * CCp + 4.0 * B * Cout * vout;
+            I.alg_bytes[1] = I.alg_bytes[3] = 0.0;
+            I.x_planes = 0;
+        }
     } else {
         I.alg_bytes[2] = 4.0 * B * C * vin + 4.0 * Cout * C * kv + 4.0 * B * Cout * vout;
         I.alg_flops[2] = I.direct_flops;
@@ -664,6 +680,7 @@ void conv_plan_options_init(conv_plan_options *o) {
     o->single_cta_mma = 0;
     o->e2e_chunks = 0;
     o->overlap_kernel_transform = -1;
+    o->fused = 0;
 }
 
 static const conv_plan_options *opts_or_default(const conv_plan_options *o, conv_plan_options *tmp) {
@@ -757,7 +774,9 @@ static conv_status plan_create(conv_plan_t *out, int nd, int B, int C, int Cout,
     conv_plan_s *p = (conv_plan_s *)calloc(1, sizeof(conv_plan_s));
     if (!p) return CONV_ERR_OUT_OF_MEMORY;
     conv_gemm_impl gemm = opts.gemm;
-    if (gemm == CONV_GEMM_AUTO) gemm = fc_tcgen05_available() ? CONV_GEMM_TCGEN05_F16X3 : CONV_GEMM_FFMA;
+    if (gemm == CONV_GEMM_AUTO)
+        gemm = !fc_tcgen05_available() ? CONV_GEMM_FFMA
+                                       : (opts.fused == 1 ? CONV_GEMM_TCGEN05_3XTF32 : CONV_GEMM_TCGEN05_F16X3);
     if ((gemm == CONV_GEMM_TCGEN05_3XTF32 || gemm == CONV_GEMM_TCGEN05_F16X3) && !fc_tcgen05_available()) {
         free(p);
         fc_set_error("tcgen05 contraction not available in this build");
@@ -1105,6 +1124,7 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, cons
         fc_set_error("bad stage %d", stage);
         return CONV_ERR_INVALID_ARG;
     }
+    if (g.fused && (stage == 1 || stage == 3)) return CONV_OK;  // inside the fused kernel (stage 2)
     switch (stage) {
         case 0: {
             int handled = 0;
@@ -1129,6 +1149,8 @@ static conv_status run_stage(conv_plan_s *p, const Geometry &g0, int stage, cons
             return launch_result(fc_launch_input_transform(g, p->d_consts, in, U, s), "NK2 input transform");
         }
         case 2:
+            if (g.fused)
+                return launch_result(fc_launch_fused_wino23(g, in, V, Vlo, out, s), "NK2-NK4 fused F(2,3)");
             if (p->gemm == CONV_GEMM_FFMA)
                 return launch_result(fc_launch_gemm_ffma(g, V, U, X, s), "NK3 FFMA contraction");
             if (g.vf16)
@@ -1643,6 +1665,10 @@ conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const in
         conv_plan_options_init(&opts);
     }
     opts.chunk_images = 0;
+    if (opts.fused) {  // the exchange needs U and X in memory
+        fc_set_error("conv_eshard_create: fused plans keep U and X on chip; element sharding needs them");
+        return CONV_ERR_UNSUPPORTED;
+    }
     int Btot = 0;
     for (int k = 0; k < world; ++k) {
         if (batch[k] < 1) {

@@ -91,6 +91,7 @@ struct Geometry {
     // element-sharded execution (conv_eshard_*): the generic NK1 writes only the transformed
     // elements e in [e_lo, e_hi), at z relative to e_lo (V of E' = e_hi - e_lo elements)
     int e_lo, e_hi;
+    int fused;  // conv_plan_options.fused: NK2-NK4 in one kernel (fused_wino.cu)
 };
 
 // Per-axis constants of an N-D plan (fp64 -> fp32 once): Winograd B^T [t][t], G [t][r],
@@ -314,6 +315,16 @@ cudaError_t fc_init_twiddles();
 cudaError_t fc_fft_xform_a(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
 cudaError_t fc_fft_xform_b(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
 cudaError_t fc_fft_xform_c(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s, int *handled);
+// cuTensorMapEncodeTiled for an fp32 tensor (map: a 64-byte-aligned CUtensorMap; dims / box
+// innermost first; strides_bytes: rank - 1 entries; swizzle_bytes 0, 32, 64 or 128)
+bool fc_tma_encode_f32(void *map, const void *ptr, int rank, const unsigned long long *dims,
+                       const unsigned long long *strides_bytes, const unsigned int *box, int swizzle_bytes);
+// NK2 + NK3 + NK4 fused for Winograd F(2,3) with the 3xTF32 contraction (fused_wino.cu,
+// conv_plan_options.fused): input -> output in one kernel, V from NK1
+bool fc_fused_wino23_eligible(const Geometry &g);
+int fc_fused_wino23_lw(int n_h, int n_w);
+cudaError_t fc_launch_fused_wino23(const Geometry &g, const float *in, const float *Vhi, const float *Vlo,
+                                   float *out, cudaStream_t s);
 cudaError_t fc_fft_twiddles_a();
 cudaError_t fc_fft_twiddles_b();
 cudaError_t fc_fft_twiddles_c();

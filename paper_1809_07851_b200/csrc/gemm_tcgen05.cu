@@ -1031,6 +1031,29 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
 
 int fc_tcgen05_available() { return get_encode() != nullptr; }
 
+bool fc_tma_encode_f32(void *map, const void *ptr, int rank, const unsigned long long *dims,
+                       const unsigned long long *strides_bytes, const unsigned int *box, int swizzle_bytes) {
+    auto enc = get_encode();
+    if (!enc || rank < 1 || rank > 5) return false;
+    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE;
+    if (swizzle_bytes == 32) swz = CU_TENSOR_MAP_SWIZZLE_32B;
+    else if (swizzle_bytes == 64) swz = CU_TENSOR_MAP_SWIZZLE_64B;
+    else if (swizzle_bytes == 128) swz = CU_TENSOR_MAP_SWIZZLE_128B;
+    else if (swizzle_bytes != 0) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) st[i] = strides_bytes[i];
+    }
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank,
+                     const_cast<void *>(ptr), d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 cudaError_t fc_launch_gemm_tcgen05(const Geometry &g, const float *Vhi, const float *Vlo, const float *U, float *X,
                                    cudaStream_t s) {
     if (!Vlo) return cudaErrorInvalidValue;

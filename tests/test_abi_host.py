@@ -267,3 +267,33 @@ def test_best_method(lib):
     assert fc.best_method(64, 64, 64, 226, 226, 3)[:2] == ("regular_fft", 14)  # VGG-1.2
     assert fc.best_method(128, 96, 256, 31, 31, 5)[0].endswith("fft")         # 5x5
     assert fc.best_method(64, 512, 512, 16, 16, 3)[:2] == ("winograd", 4)      # deep
+
+
+def test_fused_option_query():
+    """conv_plan_options.fused: eligible only for 2-D Winograd F(2,3) with the
+    3xTF32 contraction; the plan then has no U / X in its workspace and one fused stage carrying
+    input + V + output bytes (the transforms' element-wise FLOPs are unchanged)."""
+    B, C, Co, x = 4, 64, 64, 58
+    staged = fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "tcgen05")
+    fused = fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "auto", fused=1)
+    assert staged["fused"] == 0 and fused["fused"] == 1
+    assert fused["gemm"] == fc.GEMMS["tcgen05"]  # AUTO resolves to 3xTF32 for fused plans
+    assert fused["bytes_U"] == 0 and fused["bytes_X"] == 0 and fused["x_planes"] == 0
+    assert fused["workspace_bytes"] < staged["workspace_bytes"]
+    assert fused["alg_bytes"][1] == 0 and fused["alg_bytes"][3] == 0
+    Ho = x - 2
+    assert fused["alg_bytes"][2] == 4.0 * (B * C * x * x + 16 * C * Co + B * Co * Ho * Ho)
+    assert fused["alg_flops"][2] == staged["alg_flops"][2]
+    for bad in (dict(method="winograd", m=4), dict(method="regular_fft", m=6), dict(method="gauss_fft", m=6)):
+        with pytest.raises(fc.ConvError):
+            fc.plan_query(B, C, Co, x, x, 3, bad["method"], bad["m"], "auto", fused=1)
+    with pytest.raises(fc.ConvError):  # F16X3 / FFMA contractions, chunking, other kernel sizes
+        fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "f16x3", fused=1)
+    with pytest.raises(fc.ConvError):
+        fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "ffma", fused=1)
+    with pytest.raises(fc.ConvError):
+        fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "auto", fused=1, chunk_images=2)
+    with pytest.raises(fc.ConvError):
+        fc.plan_query(B, C, Co, x, x, 5, "winograd", 2, "auto", fused=1)
+    with pytest.raises(fc.ConvError):  # out of range
+        fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "auto", fused=2)
