@@ -305,6 +305,12 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
     const int nimg = min(IPC, g.B - b);
     const int ntiles = nimg * ntr * g.n_w;  // contiguous in n
     const long long nbase = ((long long)b * g.n_h + i0) * g.n_w;
+    // whole images of narrow rows per CTA (R = n_h, Wo < 48): stage the cropped planes at
+    // pitch Wo and copy each image out as one flat run -- the per-image strip copies were ~70%
+    // of the deep layer's NK4 instructions (ncu r02 deep: NK4 34 -> 18 us).  Wide rows keep
+    // the padded-pitch vector staging (VGG-3.2 F(6,3) NK4 131 -> 156 us with the cropped one).
+    const bool whole = R == g.n_h && g.Wo < 48;
+    const float inv_nh = 1.f / (float)g.n_h;
     size_t ebytes = (size_t)g.Xm * g.BN_pad * sizeof(float);
     asm("" : "+l"(ebytes));
     const float *src0 = X + (size_t)co * g.BN_pad + nbase;
@@ -326,6 +332,16 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
             },
             y);
         const int ti = fc_div(tl, g.divNw), tj = tl - ti * g.n_w;  // ti counts rows across the CTA's images
+        if (whole) {  // whole images: stage the cropped Ho x Wo planes back to back
+            const int im = fcx::fc_sdiv(ti, inv_nh), oy = (ti - im * g.n_h) * m, ox = tj * m;
+            float *q = so + ((size_t)im * g.Ho + oy) * g.Wo + ox;
+#pragma unroll
+            for (int a = 0; a < MM; ++a)
+#pragma unroll
+                for (int c = 0; c < MM; ++c)
+                    if (oy + a < g.Ho && ox + c < g.Wo) q[a * g.Wo + c] = y[a][c];
+            continue;
+        }
         float *q0 = so + ti * m * SWo + tj * m;
 #pragma unroll
         for (int a = 0; a < MM; ++a) {
@@ -345,6 +361,27 @@ __global__ void __launch_bounds__(256, 4) nk4_wino(Geometry g, int R, int IPC, i
         }
     }
     __syncthreads();
+    if (whole) {  // every image's Ho x Wo plane is one contiguous run in both places
+        const int plane = g.Ho * g.Wo;
+        float *dst0 = out + ((size_t)b * g.Cout + co) * plane;
+        const size_t istride = (size_t)g.Cout * plane;
+        if ((plane & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            const int p4 = plane >> 2;
+            const float inv = 1.f / (float)p4;
+            for (int k = threadIdx.x; k < nimg * p4; k += blockDim.x) {
+                const int im = fcx::fc_sdiv(k, inv), r4 = k - im * p4;
+                __stcs(reinterpret_cast<float4 *>(dst0 + im * istride) + r4,
+                       reinterpret_cast<const float4 *>(so)[k]);
+            }
+        } else {
+            const float inv = 1.f / (float)plane;
+            for (int k = threadIdx.x; k < nimg * plane; k += blockDim.x) {
+                const int im = fcx::fc_sdiv(k, inv), r = k - im * plane;
+                __stcs(dst0 + im * istride + r, so[k]);
+            }
+        }
+        return;
+    }
     const int y0 = i0 * m;
     const int orows = min(ntr * m, g.Ho - y0);
     for (int im = 0; im < nimg; ++im) {
@@ -523,6 +560,7 @@ cudaError_t launch_wino(const Geometry &g, const float *src, float *dst, bool fo
         }
         const int nstrip = (g.n_h + R - 1) / R;
         const int ngroup = (g.B + IPC - 1) / IPC;
+        // whole images (R = n_h): the kernel stages cropped Ho x Wo planes, at most the strip size
         const size_t smem = sizeof(float) * (size_t)IPC * R * g.m * SWo;
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
         fc_smem_attr((const void *)nk4_wino<T, MM>, 200 * 1024);
