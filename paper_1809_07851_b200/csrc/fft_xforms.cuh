@@ -156,7 +156,10 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     // (stepping these loads by an opaque byte stride, as nk4_wino does, measured slower here:
     // VGG-1.2 t = 27 / 32 NK4 +7-9%, three-plane Gauss +13%)
     const size_t hstride = (size_t)H * estride;  // k -> k+1 along the element index e = k*H + l
-    const float inv_nt = 1.f / (float)ntiles, inv_nw = 1.f / (float)g.n_w;
+    const float inv_nt = 1.f / (float)ntiles, inv_nw = 1.f / (float)g.n_w, inv_nh = 1.f / (float)g.n_h;
+    // whole images of narrow rows (R = n_h, Wo < 48): phase B stages the cropped Ho x Wo planes
+    // at pitch Wo and phase C copies each image out as one flat run (as nk4_wino)
+    const bool whole = R == g.n_h && g.Wo < 48;
     for (int it = threadIdx.x; it < H * ntiles; it += blockDim.x) {
         const int l = fc_sdiv(it, inv_nt), tl = it - l * ntiles;
         cf z[T];
@@ -202,6 +205,18 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
         }
         fct::fft<T, +1>(z);
         const int ti = fc_sdiv(tl, inv_nw), tj = tl - ti * g.n_w;  // ti counts tile rows across the CTA's images
+        if (whole) {  // cropped Ho x Wo planes back to back
+            const int im = fc_sdiv(ti, inv_nh), oy = (ti - im * g.n_h) * m + a0, ox = tj * m;
+            float *q = so + ((size_t)im * g.Ho + oy) * g.Wo + ox;
+            const bool r0 = oy < g.Ho, r1 = has1 && oy + 1 < g.Ho;
+#pragma unroll
+            for (int c = 0; c < T; ++c)
+                if (c < m && ox + c < g.Wo) {
+                    if (r0) q[c] = z[c].x;
+                    if (r1) q[g.Wo + c] = z[c].y;
+                }
+            continue;
+        }
         float *q0 = so + (size_t)(ti * m + a0) * SWo + tj * m;
         if ((m & 1) == 0 && (SWo & 1) == 0) {  // 8-byte aligned pairs
 #pragma unroll
@@ -222,6 +237,26 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
         }
     }
     __syncthreads();
+    if (whole) {  // every image's Ho x Wo plane is one contiguous run in both places
+        const int plane = g.Ho * g.Wo;
+        float *dst0 = out + ((size_t)b * g.Cout + co) * plane;
+        const size_t istride = (size_t)g.Cout * plane;
+        if ((plane & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            const int p4 = plane >> 2;
+            const float inv = 1.f / (float)p4;
+            for (int k = threadIdx.x; k < nimg * p4; k += blockDim.x) {
+                const int im = fc_sdiv(k, inv), r4 = k - im * p4;
+                __stcs(reinterpret_cast<float4 *>(dst0 + im * istride) + r4, reinterpret_cast<const float4 *>(so)[k]);
+            }
+        } else {
+            const float inv = 1.f / (float)plane;
+            for (int k = threadIdx.x; k < nimg * plane; k += blockDim.x) {
+                const int im = fc_sdiv(k, inv), r = k - im * plane;
+                __stcs(dst0 + im * istride + r, so[k]);
+            }
+        }
+        return;
+    }
     const int y0 = i0 * m;
     const int orows = min(ntr * m, g.Ho - y0);
     for (int im = 0; im < nimg; ++im) {
