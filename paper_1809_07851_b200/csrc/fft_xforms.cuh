@@ -298,7 +298,10 @@ cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool for
         constexpr int items_env = 256;
         // at least 32 tiles per CTA: each (l, c') run of X a warp loads is then >= 128 bytes
         // (VGG-1.2 m = 14 had 16-tile strips: 64-byte runs)
-        const int target = items_env / H > 32 ? items_env / H : 32;
+        // (t > 18: at least 16 -- more, smaller CTAs overlap their load and FFT phases; VGG-3.2
+        // t = 21 NK4 203 -> 158 us, t = 27 / 32 unchanged, t = 16 VGG-1.2 +3% at 16)
+        constexpr int min_tiles = T > 18 ? 16 : 32;
+        const int target = items_env / H > min_tiles ? items_env / H : min_tiles;
         int R = target / g.n_w > 0 ? target / g.n_w : 1, IPC = 1;
         if (R >= g.n_h) {
             R = g.n_h;
