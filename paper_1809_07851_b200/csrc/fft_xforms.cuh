@@ -239,20 +239,38 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
     __syncthreads();
     if (whole) {  // every image's Ho x Wo plane is one contiguous run in both places
         const int plane = g.Ho * g.Wo;
-        float *dst0 = out + ((size_t)b * g.Cout + co) * plane;
+        const bool vec = (plane & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+        const int n = vec ? plane >> 2 : plane;  // units (float4 or float) per image
         const size_t istride = (size_t)g.Cout * plane;
-        if ((plane & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-            const int p4 = plane >> 2;
-            const float inv = 1.f / (float)p4;
-            for (int k = threadIdx.x; k < nimg * p4; k += blockDim.x) {
-                const int im = fc_sdiv(k, inv), r4 = k - im * p4;
-                __stcs(reinterpret_cast<float4 *>(dst0 + im * istride) + r4, reinterpret_cast<const float4 *>(so)[k]);
+        float *dst0 = out + ((size_t)b * g.Cout + co) * plane;
+        if (n >= (int)blockDim.x) {  // planes of at least one unit per thread: a loop per image
+            float *dimg = dst0;
+            for (int i = 0; i < nimg; ++i, dimg += istride) {
+                if (vec)
+                    for (int k = threadIdx.x; k < n; k += blockDim.x)
+                        __stcs(reinterpret_cast<float4 *>(dimg) + k, reinterpret_cast<const float4 *>(so)[i * n + k]);
+                else
+                    for (int k = threadIdx.x; k < n; k += blockDim.x) __stcs(dimg + k, so[i * n + k]);
             }
-        } else {
-            const float inv = 1.f / (float)plane;
-            for (int k = threadIdx.x; k < nimg * plane; k += blockDim.x) {
-                const int im = fc_sdiv(k, inv), r = k - im * plane;
-                __stcs(dst0 + im * istride + r, so[k]);
+            return;
+        }
+        // small planes: one flat (image, unit) walk over all images, the position advancing
+        // by blockDim units per step with one division up front (a division per element was
+        // ~25 instructions per float, ncu k5 m = 9 NK4; a loop per image costs every warp its
+        // overhead per image: deep NK4 18 -> 25 us)
+        const int q = (int)blockDim.x / n, rem = (int)blockDim.x - q * n;
+        int im = (int)threadIdx.x / n, r = (int)threadIdx.x - im * n;
+        while (im < nimg) {
+            if (vec)
+                __stcs(reinterpret_cast<float4 *>(dst0 + im * istride) + r,
+                       reinterpret_cast<const float4 *>(so)[im * n + r]);
+            else
+                __stcs(dst0 + im * istride + r, so[im * n + r]);
+            im += q;
+            r += rem;
+            if (r >= n) {
+                r -= n;
+                ++im;
             }
         }
         return;
