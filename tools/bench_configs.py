@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--all-m", action="store_true", help="sweep every compiled tile size (autotuner)")
     ap.add_argument("--flush-l2", action="store_true", help="write 2x L2 between timed steps")
     ap.add_argument("--no-direct", action="store_true")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused F(2,3) kernel (conv_plan_options.fused)")
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
@@ -76,13 +77,17 @@ def main():
         runs = all_runs(cfg) if args.all_m else list(cfg.runs)
         if not args.no_direct:
             runs.append(("direct", 0))
-        for method, m in runs:
+        if cfg.r == 3 and not args.no_fused:  # the fused F(2,3) kernel beside the rest
+            runs.append(("winograd", 2, {"fused": 1}))
+        for run in runs:
+            method, m = run[0], run[1]
+            opts = run[2] if len(run) > 2 else {}
             try:
                 p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m,
-                            args.gemm if method != "direct" else "auto")
+                            (args.gemm if method != "direct" else "auto") if not opts else "auto", **opts)
                 ws = p.alloc_workspace()
             except (fc.ConvError, RuntimeError) as exc:  # e.g. a workspace beyond HBM
-                rows["%s/m=%d" % (method, m)] = {"error": str(exc)[:160]}
+                rows["%s/m=%d%s" % (method, m, "+fused" if opts else "")] = {"error": str(exc)[:160]}
                 torch.cuda.empty_cache()
                 continue
             for _ in range(3):
@@ -108,10 +113,12 @@ def main():
                 torch.cuda.synchronize()
                 ms = a.elapsed_time(b) / steps
             st = [round(v, 4) for v in p.forward_profiled(x, w, out, ws)]
-            key = "%s/m=%d" % (method, m)
+            key = "%s/m=%d%s" % (method, m, "+fused" if opts else "")
             rows[key] = {"ms": round(ms, 4), "tflops": round(cfg.direct_flops / (ms * 1e-3) / 1e12, 2),
                          "stage_ms": st, "t": p.info["t"]}
-            if method != "direct":
+            if opts:
+                rows[key]["options"] = opts
+            if method != "direct" and not opts:
                 infos[(method, m)] = p.info
                 meas[(method, m)] = ms
                 rows[key]["stage_hbm_frac"] = [round(p.info["alg_bytes"][s] / (st[s] * 1e-3) / (hbm * 1e9), 3)
