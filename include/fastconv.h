@@ -376,6 +376,32 @@ conv_status conv_eshard_forward_c(conv_eshard_t e, const void *x_recv, float *ou
                                   size_t workspace_bytes, void *stream);
 void conv_eshard_destroy(conv_eshard_t e);   /* NULL-safe */
 
+/* Peer-memory exchange (no collective library on the data path): the same steps, but each rank
+ * writes its packed U (resp. X) for peer k straight into peer k's receive buffer -- copy-engine
+ * transfers over NVLink / NVSwitch between devices, or within one device between processes --
+ * at this rank's segment (segments in rank order, the layout forward_b / forward_c read).
+ * u_recv_peer[k] / x_recv_peer[k]: the base of rank k's u_recv / x_recv buffer mapped into this
+ * process (k == rank: its own buffer), e.g. from conv_ipc_alloc / conv_ipc_open.  The caller
+ * orders the ranks: every rank's forward_a_peer (forward_b_peer) must have completed before any
+ * rank runs forward_b (forward_c), e.g. stream synchronize + a barrier.  The per-image maxima
+ * (F16X3) are still gathered by the caller.  Errors: as forward_a / forward_b; INVALID_ARG for a
+ * NULL array or entry. */
+conv_status conv_eshard_forward_a_peer(conv_eshard_t e, const float *in, const float *w, void *const *u_recv_peer,
+                                       float *umax_out, void *workspace, size_t workspace_bytes, void *stream);
+conv_status conv_eshard_forward_b_peer(conv_eshard_t e, const void *u_recv, const float *umax_all,
+                                       void *const *x_recv_peer, void *workspace, size_t workspace_bytes,
+                                       void *stream);
+
+/* Inter-process buffers for the peer exchange: conv_ipc_alloc returns device memory of the
+ * current device (cudaMalloc, `bytes` > 0) and its 64-byte IPC handle in handle_out; another
+ * process maps it with conv_ipc_open (device pointer valid in that process; peer access enabled
+ * lazily) and unmaps it with conv_ipc_close; the owner frees it with conv_ipc_free.  Errors:
+ * INVALID_ARG (NULL / zero size), OUT_OF_MEMORY, CUDA. */
+conv_status conv_ipc_alloc(size_t bytes, void **ptr, void *handle_out);
+conv_status conv_ipc_free(void *ptr);
+conv_status conv_ipc_open(const void *handle, void **ptr);
+conv_status conv_ipc_close(void *ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -147,6 +147,12 @@ def load(build_if_missing: bool = False):
         "conv_eshard_forward_b": ([vp, vp, vp, vp, vp, sz, vp], i),
         "conv_eshard_forward_c": ([vp, vp, vp, vp, sz, vp], i),
         "conv_eshard_destroy": ([vp], None),
+        "conv_eshard_forward_a_peer": ([vp, vp, vp, ctypes.POINTER(vp), vp, vp, sz, vp], i),
+        "conv_eshard_forward_b_peer": ([vp, vp, vp, ctypes.POINTER(vp), vp, sz, vp], i),
+        "conv_ipc_alloc": ([sz, ctypes.POINTER(vp), vp], i),
+        "conv_ipc_free": ([vp], i),
+        "conv_ipc_open": ([vp, ctypes.POINTER(vp)], i),
+        "conv_ipc_close": ([vp], i),
         "conv_plan_backward": ([ctypes.POINTER(vp)] + [i] * 9 + [ctypes.POINTER(PlanOptions)], i),
         "conv_backward_data": ([vp, vp, vp, vp, vp, sz, vp], i),
         "conv_backward_filter": ([vp, vp, vp, vp, vp, sz, vp], i),
@@ -473,9 +479,24 @@ class EShard:
         _check(load().conv_eshard_forward_b(self._h, u_recv.data_ptr(), umax_all.data_ptr(), x_send.data_ptr(),
                                             workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream)))
 
+    def forward_a_peer(self, x, w, u_recv_peers, umax_out, workspace, stream=None):
+        """u_recv_peers: per rank k, the device address (int) of rank k's u_recv buffer mapped
+        into this process (IPCBuffer.peer_ptrs)."""
+        _check_tensor(x, "input", self.in_shape)
+        _check_tensor(w, "weights", self.w_shape)
+        arr = (ctypes.c_void_p * self.world)(*u_recv_peers)
+        _check(load().conv_eshard_forward_a_peer(self._h, x.data_ptr(), w.data_ptr(), arr, umax_out.data_ptr(),
+                                                 workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream)))
+
+    def forward_b_peer(self, u_recv_ptr, umax_all, x_recv_peers, workspace, stream=None):
+        arr = (ctypes.c_void_p * self.world)(*x_recv_peers)
+        _check(load().conv_eshard_forward_b_peer(self._h, u_recv_ptr, umax_all.data_ptr(), arr,
+                                                 workspace.data_ptr(), _nbytes(workspace), _stream_ptr(stream)))
+
     def forward_c(self, x_recv, out, workspace, stream=None):
         _check_tensor(out, "out", self.out_shape)
-        _check(load().conv_eshard_forward_c(self._h, x_recv.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+        xr = x_recv if isinstance(x_recv, int) else x_recv.data_ptr()  # tensor or IPCBuffer.ptr
+        _check(load().conv_eshard_forward_c(self._h, xr, out.data_ptr(), workspace.data_ptr(),
                                             _nbytes(workspace), _stream_ptr(stream)))
 
     def __del__(self):
@@ -483,6 +504,35 @@ class EShard:
         if h is not None and h.value and _lib is not None:
             _lib.conv_eshard_destroy(h)
             self._h = None
+
+
+class IPCBuffer:
+    """Device memory shareable between processes (conv_ipc_alloc): `handle` (64 bytes) goes to
+    the peers, which map it with IPCBuffer.open(handle); `ptr` is this process's address."""
+
+    def __init__(self, nbytes: int):
+        lib = load()
+        p = ctypes.c_void_p()
+        h = (ctypes.c_char * 64)()
+        _check(lib.conv_ipc_alloc(max(int(nbytes), 16), ctypes.byref(p), h))
+        self.ptr, self.handle, self.nbytes, self._owned = int(p.value), bytes(h), int(nbytes), True
+
+    @staticmethod
+    def open(handle: bytes) -> int:
+        """Map a peer's buffer; returns its device address in this process."""
+        p = ctypes.c_void_p()
+        h = (ctypes.c_char * 64).from_buffer_copy(handle)
+        _check(load().conv_ipc_open(h, ctypes.byref(p)))
+        return int(p.value)
+
+    @staticmethod
+    def close(ptr: int):
+        _check(load().conv_ipc_close(ctypes.c_void_p(ptr)))
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and _lib is not None:
+            _lib.conv_ipc_free(ctypes.c_void_p(self.ptr))
+            self._owned = False
 
 
 class Graph:

@@ -1648,6 +1648,20 @@ struct conv_eshard_s {
 
 static int split_lo(int n, int k, int w) { return k * (n / w) + (k < n % w ? k : n % w); }
 
+// byte offset of sender j's segment in receiver k's U / X receive buffer (segments in rank order)
+static size_t eshard_u_recv_off(const conv_eshard_s *e, int k, int j) {
+    const Geometry &g = e->lp->g;
+    size_t off = 0;
+    for (int i = 0; i < j; ++i) off += (size_t)(e->bnpad[i] / FC_TB) * e->pu * e->ecnt[k] * g.K * FC_TB * 4;
+    return off;
+}
+static size_t eshard_x_recv_off(const conv_eshard_s *e, int k, int j) {
+    const Geometry &g = e->lp->g;
+    size_t off = 0;
+    for (int i = 0; i < j; ++i) off += (size_t)e->px * e->ecnt[i] * g.Xm * e->bnpad[k] * 4;
+    return off;
+}
+
 extern "C" {
 
 conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const int *batch, int C, int Cout, int H,
@@ -1833,13 +1847,21 @@ static conv_status eshard_check(conv_eshard_s *e, void *ws, size_t ws_bytes) {
     return check_dev_ptr(e->lp, ws, "workspace");
 }
 
-conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float *w, void *u_send, float *umax_out,
-                                  void *ws, size_t ws_bytes, void *stream) {
+static conv_status eshard_forward_a_impl(conv_eshard_t e, const float *in, const float *w, void *u_send,
+                                         void *const *u_recv_peer, float *umax_out, void *ws, size_t ws_bytes,
+                                         void *stream) {
     conv_status st = eshard_check(e, ws, ws_bytes);
     if (st) return st;
-    if ((st = check_dev_ptr(e->lp, in, "in")) || (st = check_dev_ptr(e->lp, w, "weights")) ||
-        (st = check_dev_ptr(e->lp, u_send, "u_send")))
+    if ((st = check_dev_ptr(e->lp, in, "in")) || (st = check_dev_ptr(e->lp, w, "weights"))) return st;
+    if (u_recv_peer) {
+        for (int k = 0; k < e->world; ++k)
+            if (!u_recv_peer[k]) {
+                fc_set_error("u_recv_peer[%d] is NULL", k);
+                return CONV_ERR_INVALID_ARG;
+            }
+    } else if ((st = check_dev_ptr(e->lp, u_send, "u_send"))) {
         return st;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     char *b = (char *)ws;
     conv_plan_s *lp = e->lp;
@@ -1868,13 +1890,15 @@ conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float 
             st = launch_result(cudaMemsetAsync(umax_out, 0, (size_t)lp->g.B * 4, s), "max|U_b| clear");
         if (st) return st;
     }
-    // pack U_local [NB][Z][K][128] -> peer j: [NB][pu][E_j][K][128]
+    // pack U_local [NB][Z][K][128] -> peer j: [NB][pu][E_j][K][128], into the send buffer
+    // (peer-major) or straight into peer j's receive buffer at this rank's segment
     const Geometry &g = lp->g;
     const size_t row = (size_t)g.K * FC_TB * 4;  // one (z) slab of a 128-tile block
     const long long NB = e->bnpad[e->rank] / FC_TB;
     char *dst = (char *)u_send;
     for (int j = 0; j < e->world; ++j) {
         const int Ej = e->ecnt[j];
+        if (u_recv_peer) dst = (char *)u_recv_peer[j] + eshard_u_recv_off(e, j, e->rank);
         for (int p = 0; p < e->pu; ++p) {
             const char *src = b + e->off_U + (size_t)(p * g.E + e->elo[j]) * row;
             st = launch_result(cudaMemcpy2DAsync(dst + (size_t)p * Ej * row, (size_t)e->pu * Ej * row, src,
@@ -1886,6 +1910,20 @@ conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float 
         dst += e->u_send[j];
     }
     return CONV_OK;
+}
+
+conv_status conv_eshard_forward_a(conv_eshard_t e, const float *in, const float *w, void *u_send, float *umax_out,
+                                  void *ws, size_t ws_bytes, void *stream) {
+    return eshard_forward_a_impl(e, in, w, u_send, nullptr, umax_out, ws, ws_bytes, stream);
+}
+
+conv_status conv_eshard_forward_a_peer(conv_eshard_t e, const float *in, const float *w, void *const *u_recv_peer,
+                                       float *umax_out, void *ws, size_t ws_bytes, void *stream) {
+    if (!u_recv_peer) {
+        fc_set_error("NULL u_recv_peer array");
+        return CONV_ERR_INVALID_ARG;
+    }
+    return eshard_forward_a_impl(e, in, w, nullptr, u_recv_peer, umax_out, ws, ws_bytes, stream);
 }
 
 }  // extern "C"
@@ -1907,11 +1945,20 @@ __global__ void eshard_col_umax(unsigned int *col, const unsigned int *img, cons
 
 extern "C" {
 
-conv_status conv_eshard_forward_b(conv_eshard_t e, const void *u_recv, const float *umax_all, void *x_send, void *ws,
-                                  size_t ws_bytes, void *stream) {
+static conv_status eshard_forward_b_impl(conv_eshard_t e, const void *u_recv, const float *umax_all, void *x_send,
+                                         void *const *x_recv_peer, void *ws, size_t ws_bytes, void *stream) {
     conv_status st = eshard_check(e, ws, ws_bytes);
     if (st) return st;
-    if ((st = check_dev_ptr(e->lp, u_recv, "u_recv")) || (st = check_dev_ptr(e->lp, x_send, "x_send"))) return st;
+    if ((st = check_dev_ptr(e->lp, u_recv, "u_recv"))) return st;
+    if (x_recv_peer) {
+        for (int k = 0; k < e->world; ++k)
+            if (!x_recv_peer[k]) {
+                fc_set_error("x_recv_peer[%d] is NULL", k);
+                return CONV_ERR_INVALID_ARG;
+            }
+    } else if ((st = check_dev_ptr(e->lp, x_send, "x_send"))) {
+        return st;
+    }
     cudaStream_t s = (cudaStream_t)stream;
     char *b = (char *)ws;
     conv_plan_s *lp = e->lp;
@@ -1944,17 +1991,88 @@ conv_status conv_eshard_forward_b(conv_eshard_t e, const void *u_recv, const flo
     else
         st = launch_result(fc_launch_gemm_tcgen05(gj, V, Vlo, U, Xj, s), "NK3 3xTF32 contraction (element shard)");
     if (st) return st;
-    // pack X_j [Xz_j][Xm][bn_tot] -> peer k: [Xz_j][Xm][bnpad_k] (its images' columns)
+    // pack X_j [Xz_j][Xm][bn_tot] -> peer k: [Xz_j][Xm][bnpad_k] (its images' columns), into
+    // the send buffer or straight into peer k's receive buffer at this rank's segment
     char *dst = (char *)x_send;
     long long col0 = 0;
     for (int k = 0; k < e->world; ++k) {
         const size_t wbytes = (size_t)e->bnpad[k] * 4;
+        if (x_recv_peer) dst = (char *)x_recv_peer[k] + eshard_x_recv_off(e, k, e->rank);
         st = launch_result(cudaMemcpy2DAsync(dst, wbytes, (const char *)Xj + col0 * 4, (size_t)e->bn_tot * 4, wbytes,
                                              (size_t)gj.Xz * gj.Xm, cudaMemcpyDeviceToDevice, s),
                            "X pack");
         if (st) return st;
         dst += e->x_send[k];
         col0 += e->bnpad[k];
+    }
+    return CONV_OK;
+}
+
+conv_status conv_eshard_forward_b(conv_eshard_t e, const void *u_recv, const float *umax_all, void *x_send, void *ws,
+                                  size_t ws_bytes, void *stream) {
+    return eshard_forward_b_impl(e, u_recv, umax_all, x_send, nullptr, ws, ws_bytes, stream);
+}
+
+conv_status conv_eshard_forward_b_peer(conv_eshard_t e, const void *u_recv, const float *umax_all,
+                                       void *const *x_recv_peer, void *ws, size_t ws_bytes, void *stream) {
+    if (!x_recv_peer) {
+        fc_set_error("NULL x_recv_peer array");
+        return CONV_ERR_INVALID_ARG;
+    }
+    return eshard_forward_b_impl(e, u_recv, umax_all, nullptr, x_recv_peer, ws, ws_bytes, stream);
+}
+
+// Inter-process exchange buffers: device memory from cudaMalloc (so an IPC handle covers the
+// buffer from its first byte) and its handle; a peer process maps it with conv_ipc_open.
+conv_status conv_ipc_alloc(size_t bytes, void **ptr, void *handle_out) {
+    if (!ptr || !handle_out || bytes == 0) {
+        fc_set_error("conv_ipc_alloc: NULL argument or zero size");
+        return CONV_ERR_INVALID_ARG;
+    }
+    *ptr = nullptr;
+    cudaError_t ce = cudaMalloc(ptr, bytes);
+    if (ce == cudaSuccess) ce = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(handle_out), *ptr);
+    if (ce != cudaSuccess) {
+        if (*ptr) cudaFree(*ptr);
+        *ptr = nullptr;
+        fc_set_error("conv_ipc_alloc: %s", cudaGetErrorString(ce));
+        return ce == cudaErrorMemoryAllocation ? CONV_ERR_OUT_OF_MEMORY : CONV_ERR_CUDA;
+    }
+    return CONV_OK;
+}
+
+conv_status conv_ipc_free(void *ptr) {
+    if (!ptr) return CONV_OK;
+    const cudaError_t ce = cudaFree(ptr);
+    if (ce != cudaSuccess) {
+        fc_set_error("conv_ipc_free: %s", cudaGetErrorString(ce));
+        return CONV_ERR_CUDA;
+    }
+    return CONV_OK;
+}
+
+conv_status conv_ipc_open(const void *handle, void **ptr) {
+    if (!handle || !ptr) {
+        fc_set_error("conv_ipc_open: NULL argument");
+        return CONV_ERR_INVALID_ARG;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    const cudaError_t ce = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (ce != cudaSuccess) {
+        *ptr = nullptr;
+        fc_set_error("conv_ipc_open: %s", cudaGetErrorString(ce));
+        return CONV_ERR_CUDA;
+    }
+    return CONV_OK;
+}
+
+conv_status conv_ipc_close(void *ptr) {
+    if (!ptr) return CONV_OK;
+    const cudaError_t ce = cudaIpcCloseMemHandle(ptr);
+    if (ce != cudaSuccess) {
+        fc_set_error("conv_ipc_close: %s", cudaGetErrorString(ce));
+        return CONV_ERR_CUDA;
     }
     return CONV_OK;
 }

@@ -145,3 +145,59 @@ def eshard_forward(es, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, ws: 
         bufs["x_recv"][:sum(es.x_recv)].copy_(bufs["x_send"][:sum(es.x_send)])
     es.forward_c(bufs["x_recv"], out, ws)
     return bufs
+
+
+def eshard_forward_p2p(es, x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, ws: torch.Tensor,
+                       bufs: dict | None = None, host_staging: bool = False) -> dict:
+    """Element-sharded forward with the U / X exchange over peer memory instead of a collective
+    (conv_eshard_forward_a_peer / _b_peer): every rank's receive buffers are IPC-shared device
+    memory mapped into every other rank, each rank copies its packed U (X) straight into the
+    owners' buffers, and a stream synchronize + barrier orders the phases.  Only the per-image
+    F16X3 maxima (a few bytes) still travel through all_gather.  Same results as
+    eshard_forward, bit for bit."""
+    import paper_1809_07851_b200 as fc
+    dev = x.device
+    world, rank = es.world, es.rank
+    if bufs is None:
+        u, xr = fc.IPCBuffer(sum(es.u_recv)), fc.IPCBuffer(sum(es.x_recv))
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, (u.handle, xr.handle))
+        else:
+            handles = [(u.handle, xr.handle)]
+        up = [u.ptr if k == rank else fc.IPCBuffer.open(handles[k][0]) for k in range(world)]
+        xp = [xr.ptr if k == rank else fc.IPCBuffer.open(handles[k][1]) for k in range(world)]
+        bufs = {"u_buf": u, "x_buf": xr, "u_peers": up, "x_peers": xp,
+                "umax": torch.zeros(max(es.batch), dtype=torch.float32, device=dev),
+                "umax_all": torch.zeros(sum(es.batch), dtype=torch.float32, device=dev)}
+    stream = torch.cuda.current_stream(dev)
+    es.forward_a_peer(x, w, bufs["u_peers"], bufs["umax"], ws)
+    if world > 1:
+        stream.synchronize()  # this rank's U segments have landed in every peer
+        parts = [torch.zeros_like(bufs["umax"]) for _ in range(world)]
+        if host_staging:
+            cp = [p.cpu() for p in parts]
+            dist.all_gather(cp, bufs["umax"].cpu())
+            parts = [p.to(dev) for p in cp]
+        else:
+            dist.all_gather(parts, bufs["umax"])
+        bufs["umax_all"].copy_(torch.cat([parts[k][:es.batch[k]] for k in range(world)]))
+        dist.barrier()  # ... and every peer's in this rank's buffer
+    else:
+        bufs["umax_all"].copy_(bufs["umax"][:es.batch[0]])
+    es.forward_b_peer(bufs["u_buf"].ptr, bufs["umax_all"], bufs["x_peers"], ws)
+    if world > 1:
+        stream.synchronize()
+        dist.barrier()
+    es.forward_c(bufs["x_buf"].ptr, out, ws)
+    return bufs
+
+
+def eshard_release(bufs: dict):
+    """Unmap the peers' buffers of eshard_forward_p2p (the own buffers free with `bufs`)."""
+    import paper_1809_07851_b200 as fc
+    for key, own in (("u_peers", "u_buf"), ("x_peers", "x_buf")):
+        for p in bufs.get(key, []):
+            if p != bufs[own].ptr:
+                fc.IPCBuffer.close(p)
+    bufs.clear()

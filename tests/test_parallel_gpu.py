@@ -118,7 +118,7 @@ ES_RUNS = [("winograd", 4, {}), ("regular_fft", 6, {}), ("regular_fft", 6, {"com
            ("gauss_fft", 8, {"gauss_combine": 0}), ("gauss_fft", 8, {"gauss_combine": 1})]
 
 
-def _es_worker(rank, world, port, shape, batch, q):
+def _es_worker(rank, world, port, shape, batch, q, p2p=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     import synth
@@ -139,7 +139,14 @@ def _es_worker(rank, world, port, shape, batch, q):
                 es = fc.EShard(world, rank, batch, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm, **opts)
                 ws = es.alloc_workspace()
                 y = torch.empty(es.out_shape, device="cuda")
-                parallel.eshard_forward(es, x, w, y, ws, host_staging=True)
+                if p2p:  # exchange through IPC-shared receive buffers (conv_eshard_forward_*_peer)
+                    bufs = parallel.eshard_forward_p2p(es, x, w, y, ws, host_staging=True)
+                    parallel.eshard_forward_p2p(es, x, w, y, ws, bufs=bufs, host_staging=True)  # buffers reused
+                    torch.cuda.synchronize()
+                    parallel.barrier()
+                    parallel.eshard_release(bufs)
+                else:
+                    parallel.eshard_forward(es, x, w, y, ws, host_staging=True)
                 torch.cuda.synchronize()
                 ref = fc.Plan(batch[rank], cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm,
                               **opts).forward(x, w)
@@ -157,20 +164,23 @@ def _es_worker(rank, world, port, shape, batch, q):
             torch.distributed.destroy_process_group()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("shape,batch", [((5, 32, 256, 18, 18, 3), (3, 2)), ((4, 24, 64, 20, 17, 3), (1, 3)),
                                          ((3, 16, 32, 14, 14, 3), (3,))])
-def test_element_sharded_equals_unsharded(shape, batch):
+def test_element_sharded_equals_unsharded(shape, batch, p2p):
     """element-sharded forwards (rank j: elements [e0_j, e1_j) of every image,
     the transforms of its own images; all-to-alls of U and X) give each rank's images exactly
     the unsharded forward's output -- every contraction mode and method, complex mode on
-    and off, Gauss three-plane and combined."""
+    and off, Gauss three-plane and combined.  p2p: the exchange writes straight into the
+    peers' IPC-mapped receive buffers instead of a collective (two processes on one device
+    here; peer copies over NVLink across devices)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     world = len(batch)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_es_worker, args=(r, world, port, shape, batch, q)) for r in range(world)]
+    procs = [ctx.Process(target=_es_worker, args=(r, world, port, shape, batch, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=600) for _ in range(world)]
