@@ -377,6 +377,9 @@ def main():
     ap.add_argument("--mode", default="batch", choices=["batch", "eshard"],
                     help="batch-sharded ranks (no data-path collective) or element-sharded ranks "
                          "(all-to-alls of U and X, SURVEY 8(f)3); eshard needs --method and --m")
+    ap.add_argument("--exchange", default="collective", choices=["collective", "p2p"],
+                    help="eshard: U / X through all_to_all, or copied straight into the peers' "
+                         "IPC-mapped receive buffers (conv_eshard_forward_*_peer)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -662,14 +665,14 @@ def run_eshard(args, fc, parallel, base, gcfg, cfg, I_all_shape, x, w, dev, stre
     ws = es.alloc_workspace(dev)
     out = torch.empty(es.out_shape, device=dev)
     host = oversub or not torch.distributed.is_initialized() or torch.distributed.get_backend() != "nccl"
-    bufs = parallel.eshard_forward(es, x, w, out, ws, host_staging=host and world > 1)
+    fwd = parallel.eshard_forward_p2p if args.exchange == "p2p" else parallel.eshard_forward
+    bufs = fwd(es, x, w, out, ws, host_staging=host and world > 1)
     for _ in range(args.warmup):
-        parallel.eshard_forward(es, x, w, out, ws, bufs, host_staging=host and world > 1)
+        fwd(es, x, w, out, ws, bufs, host_staging=host and world > 1)
     torch.cuda.synchronize()
     parallel.barrier()
     t0 = time.time()
-    total, per = timer_fn.run(args.steps, lambda: parallel.eshard_forward(es, x, w, out, ws, bufs,
-                                                                          host_staging=host and world > 1))
+    total, per = timer_fn.run(args.steps, lambda: fwd(es, x, w, out, ws, bufs, host_staging=host and world > 1))
     torch.cuda.synchronize()
     parallel.barrier()
     t1 = time.time()
@@ -686,10 +689,13 @@ def run_eshard(args, fc, parallel, base, gcfg, cfg, I_all_shape, x, w, dev, stre
                 "config": {"workload": base.name, "global_batch": gcfg.B, "B_per_gpu": cfg.B, "C": cfg.C,
                            "Cout": cfg.Cout, "H": cfg.H, "W": cfg.W, "r": cfg.r, "method": args.method, "m": args.m,
                            "gemm": fc.GEMM_NAMES.get(es.info["gemm"], args.gemm),
-                           "parallelism": "es%d (element-sharded: elements [e0, e1) of every image per rank; "
-                                          "all-to-all of U and X, all-gather of per-image maxima%s)" % (
-                                              world, ", staged through the host (gloo)" if host and world > 1 else
-                                              ", NCCL" if world > 1 else ""),
+                           "parallelism": "es%d (element-sharded: elements [e0, e1) of every image per rank; %s)" % (
+                               world, ("U and X copied into the peers' IPC-mapped receive buffers, all-gather of "
+                                       "per-image maxima" if args.exchange == "p2p" else
+                                       "all-to-all of U and X, all-gather of per-image maxima" +
+                                       (", staged through the host (gloo)" if host and world > 1 else
+                                        ", NCCL" if world > 1 else ""))),
+                           "exchange": args.exchange,
                            "elements_per_rank": es.e_count, "E": es.info["E"],
                            "bytes_exchanged_per_rank": {"u_send": sum(es.u_send), "x_send": sum(es.x_send)},
                            "l2": "flushed between steps" if flush else "no flush (%.0f MB/GPU)" % (io_bytes / 1e6),

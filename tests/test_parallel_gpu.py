@@ -193,8 +193,8 @@ def test_element_sharded_equals_unsharded(shape, batch, p2p):
     assert all(p.exitcode == 0 for p in procs)
 
 
-@pytest.mark.parametrize("gpus", [1, 2])
-def test_bench_eshard_mode(gpus):
+@pytest.mark.parametrize("gpus,exchange", [(1, "collective"), (2, "collective"), (2, "p2p")])
+def test_bench_eshard_mode(gpus, exchange):
     """bench.py --mode eshard prints one line per run: deep layer, FFT m = 14,
     element shards of E = 144 over the ranks."""
     if not torch.cuda.is_available():
@@ -203,10 +203,12 @@ def test_bench_eshard_mode(gpus):
     env.pop("WORLD_SIZE", None)
     res = subprocess.run([sys.executable, "bench.py", "--gpus", str(gpus), "--steps", "3", "--warmup", "3",
                           "--workload", "deep", "--mode", "eshard", "--method", "regular_fft", "--m", "14",
-                          "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+                          "--exchange", exchange, "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900, env=env)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = [l for l in res.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, res.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == gpus and d["value"] > 0 and d["config"]["parallelism"].startswith("es%d" % gpus)
     assert d["config"]["E"] == 144 and d["config"]["elements_per_rank"] == 144 // gpus
+    assert d["config"]["exchange"] == exchange
