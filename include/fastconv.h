@@ -383,9 +383,12 @@ void conv_eshard_destroy(conv_eshard_t e);   /* NULL-safe */
  * u_recv_peer[k] / x_recv_peer[k]: the base of rank k's u_recv / x_recv buffer mapped into this
  * process (k == rank: its own buffer), e.g. from conv_ipc_alloc / conv_ipc_open.  The caller
  * orders the ranks: every rank's forward_a_peer (forward_b_peer) must have completed before any
- * rank runs forward_b (forward_c), e.g. stream synchronize + a barrier.  The per-image maxima
- * (F16X3) are still gathered by the caller.  Errors: as forward_a / forward_b; INVALID_ARG for a
- * NULL array or entry. */
+ * rank runs forward_b (forward_c), e.g. stream synchronize + a barrier.  With a tcgen05
+ * contraction (not the Gauss epilogue combine) and world <= 8, forward_b_peer's contraction
+ * epilogue itself TMA-stores every 32-column X box into its owner's buffer (per-peer tensor
+ * maps): the GEMM and the X exchange are one kernel.  The per-image maxima (F16X3) are still
+ * gathered by the caller.  Errors: as forward_a / forward_b; INVALID_ARG for a NULL array or
+ * entry. */
 conv_status conv_eshard_forward_a_peer(conv_eshard_t e, const float *in, const float *w, void *const *u_recv_peer,
                                        float *umax_out, void *workspace, size_t workspace_bytes, void *stream);
 conv_status conv_eshard_forward_b_peer(conv_eshard_t e, const void *u_recv, const float *umax_all,

@@ -1639,6 +1639,7 @@ struct conv_eshard_s {
     conv_plan_s *lp;                      // local plan: this rank's images, all E (NK2 / NK4)
     conv_plan_s lpx;                      // the same plan with this workspace's U / X / max offsets
     char *d_seg;                          // device table: per-peer column offset, B_k N, first image
+    char *d_peer;                         // device: up to 8 peer X tensor maps (128 B each) + first columns
     Geometry gv;                          // NK1 over [e0, e1) (generic kernel, full-E indices)
     Geometry gj;                          // NK3 on E_j elements, bn_tot columns (N = 1)
     int pu, px;                           // plane groups of U / X (3 for Gauss three-plane, else 1)
@@ -1787,6 +1788,11 @@ conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const in
             return CONV_ERR_CUDA;
         }
     }
+    // tensor maps of the peers' X receive buffers (contraction epilogue -> peers), world <= 8
+    if (world <= 8 && cudaMalloc(&e->d_peer, 8 * 128 + 8 * 8) != cudaSuccess) {
+        cudaGetLastError();
+        e->d_peer = nullptr;  // the peer exchange then packs X with copies
+    }
     // per-peer message sizes (bytes)
     const long long NBme = e->bnpad[rank] / FC_TB;
     for (int k = 0; k < world; ++k) {
@@ -1802,6 +1808,7 @@ conv_status conv_eshard_create(conv_eshard_t *out, int world, int rank, const in
 void conv_eshard_destroy(conv_eshard_t e) {
     if (!e) return;
     if (e->d_seg) cudaFree(e->d_seg);
+    if (e->d_peer) cudaFree(e->d_peer);
     conv_destroy(e->lp);
     delete e;
 }
@@ -1984,13 +1991,43 @@ static conv_status eshard_forward_b_impl(conv_eshard_t e, const void *u_recv, co
         if ((st = launch_result(cudaGetLastError(), "per-column maxima"))) return st;
         gj.umax = col;
     }
+    // peer exchange with a tcgen05 contraction (not the Gauss combine): the epilogue stores each
+    // X box straight into its owner's receive buffer through per-peer tensor maps
+    const bool fuse_x = x_recv_peer && e->d_peer && lp->gemm != CONV_GEMM_FFMA && !gj.gc;
+    if (fuse_x) {
+        alignas(64) unsigned char maps[8][128];
+        long long cols[8];
+        long long c0 = 0;
+        for (int k = 0; k < e->world; ++k) {
+            const unsigned long long bp = (unsigned long long)e->bnpad[k];
+            const unsigned long long dims[3] = {bp, (unsigned long long)gj.Xm, (unsigned long long)gj.Xz};
+            const unsigned long long strides[2] = {bp * 4ull, (unsigned long long)gj.Xm * bp * 4ull};
+            const unsigned int box[3] = {32, 32, 1};
+            if (!fc_tma_encode_f32(maps[k], (char *)x_recv_peer[k] + eshard_x_recv_off(e, k, e->rank), 3, dims,
+                                   strides, box, 128)) {
+                fc_set_error("tensor map of peer %d's X receive buffer", k);
+                return CONV_ERR_CUDA;
+            }
+            cols[k] = c0;
+            c0 += e->bnpad[k];
+        }
+        if ((st = launch_result(cudaMemcpyAsync(e->d_peer, maps, (size_t)e->world * 128, cudaMemcpyHostToDevice, s),
+                                "peer tensor maps")) ||
+            (st = launch_result(cudaMemcpyAsync(e->d_peer + 8 * 128, cols, (size_t)e->world * 8,
+                                                cudaMemcpyHostToDevice, s),
+                                "peer columns")))
+            return st;
+        gj.peer_maps = e->d_peer;
+        gj.peer_col = (const long long *)(e->d_peer + 8 * 128);
+        gj.npeer = e->world;
+    }
     if (lp->gemm == CONV_GEMM_FFMA)
         st = launch_result(fc_launch_gemm_ffma(gj, V, U, Xj, s), "NK3 FFMA contraction (element shard)");
     else if (gj.vf16)
         st = launch_result(fc_launch_gemm_tcgen05_f16(gj, V, Vlo, U, Xj, s), "NK3 F16X3 contraction (element shard)");
     else
         st = launch_result(fc_launch_gemm_tcgen05(gj, V, Vlo, U, Xj, s), "NK3 3xTF32 contraction (element shard)");
-    if (st) return st;
+    if (st || fuse_x) return st;
     // pack X_j [Xz_j][Xm][bn_tot] -> peer k: [Xz_j][Xm][bnpad_k] (its images' columns), into
     // the send buffer or straight into peer k's receive buffer at this rank's segment
     char *dst = (char *)x_send;

@@ -92,6 +92,12 @@ struct Geometry {
     // elements e in [e_lo, e_hi), at z relative to e_lo (V of E' = e_hi - e_lo elements)
     int e_lo, e_hi;
     int fused;  // conv_plan_options.fused: NK2-NK4 in one kernel (fused_wino.cu)
+    // element-shard peer exchange (conv_eshard_forward_b_peer): the tcgen05 contraction stores
+    // each 32-column X box straight into its owner's receive buffer; device arrays of npeer
+    // tensor maps and first columns (0: the plan's own X)
+    const void *peer_maps;
+    const long long *peer_col;
+    int npeer;
 };
 
 // Per-axis constants of an N-D plan (fp64 -> fp32 once): Winograd B^T [t][t], G [t][r],

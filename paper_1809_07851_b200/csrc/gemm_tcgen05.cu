@@ -198,6 +198,31 @@ struct Tc<2> {
           "=r"(v[30]), "=r"(v[31])                                                                                \
         : "r"(taddr))
 
+// X stores of an element-sharded contraction (conv_eshard_forward_b_peer): the 32-column box
+// at column `col` of the local column space goes to the owner of that column -- peer k's
+// receive buffer, through its own tensor map (maps / col: device arrays of n entries, col[k] =
+// first column of peer k's segment); n == 0: the plan's own X (tmX).  The exchange is then
+// part of the contraction's epilogue: no local X, no pack copies.
+struct PeerX {
+    const CUtensorMap *maps;
+    const long long *col;
+    int n;
+};
+__device__ __forceinline__ void store_x_box(const CUtensorMap *tmX, const PeerX &px, uint32_t sb, int col, int row,
+                                            int z) {
+    const CUtensorMap *m = tmX;
+    int c0 = col;
+    if (px.n) {
+        int k = 0;
+        while (k + 1 < px.n && col >= px.col[k + 1]) ++k;
+        m = px.maps + k;
+        c0 = col - (int)px.col[k];
+    }
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m), "r"(sb),
+                 "r"(c0), "r"(row), "r"(z)
+                 : "memory");
+}
+
 template <int CG, int BLOCK_N, int STAGES, int BK>
 struct TcCfg {
     static constexpr int BM = 128 * CG;       // MMA M (rows of V per tile)
@@ -215,7 +240,7 @@ template <int CG, int BLOCK_N, int STAGES, int BK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     nk3_gemm_tcgen05(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                      const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int M,
-                     int K, long long NP, int Z, int cplx, int Mh, int kb_half) {
+                     int K, long long NP, int Z, int cplx, int Mh, int kb_half, PeerX px) {
     using Cfg = TcCfg<CG, BLOCK_N, STAGES, BK>;
     using I = Tc<CG>;
     static_assert(BK == 16 || BK == 32, "BK is one 64 B or 128 B swizzle row");
@@ -386,11 +411,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
-                    asm volatile(
-                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                            &tmX),
-                        "r"(sb), "r"(n0 + 32 * c), "r"(row0), "r"(z)
-                        : "memory");
+                    store_x_box(&tmX, px, sb, n0 + 32 * c, row0, z);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 buf ^= 1;
@@ -497,7 +518,7 @@ __global__ void __launch_bounds__(F16_THREADS, 1)
                          const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, int M,
                          int K, long long NP, int Z, int cplx, int Mh, int kb_half, int Cout,
                          const unsigned int *__restrict__ umax_p, const float *__restrict__ inv_sv, FastDiv divN,
-                         int BNr) {
+                         int BNr, PeerX px) {
     using Cfg = TcCfgF16<CG, BLOCK_N, SA, SU, GC>;
     using I = Tc<CG>;
     constexpr int BK = Cfg::BK, NACC = Cfg::NACC, SUB = Cfg::SUB;
@@ -784,11 +805,7 @@ __global__ void __launch_bounds__(F16_THREADS, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
-                    asm volatile(
-                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                            &tmX),
-                        "r"(sb), "r"(n0 + 32 * c), "r"(row0), "r"(z)
-                        : "memory");
+                    store_x_box(&tmX, px, sb, n0 + 32 * c, row0, z);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
                 buf ^= 1;
@@ -961,7 +978,8 @@ cudaError_t launch(const Geometry &g, const float *Vhi, const float *Vlo, const 
     long long NP_ = g.BN_pad;
     int cplx_ = g.cplx, Mh_ = g.Cout, kbh_ = (g.C + BK - 1) / BK;
     if (g.cplx && (g.Cout % Cfg::BM != 0 || g.C % BK != 0)) return cudaErrorInvalidValue;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_);
+    const PeerX px{reinterpret_cast<const CUtensorMap *>(g.peer_maps), g.peer_col, g.npeer};
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mB, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, px);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -986,6 +1004,7 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
                    CU_TENSOR_MAP_SWIZZLE_128B))
         return cudaErrorInvalidValue;
     if (GC && (g.Z != 3 * g.E || g.Xm != 2 * g.Cout || g.Cout % 32 != 0)) return cudaErrorInvalidValue;
+    if (GC && g.npeer) return cudaErrorInvalidValue;  // the combine epilogue stores through tmX only
     auto kern = nk3_gemm_tcgen05_f16<CG, BLOCK_N, SA, SU, GC>;
     {
         cudaError_t e = fc_smem_attr((const void *)kern, Cfg::SMEM_BYTES);
@@ -1022,7 +1041,8 @@ cudaError_t launch_f16(const Geometry &g, const void *Vhi, const void *Vlo, cons
     const FastDiv dN = g.divN;
     const int BNr = (int)g.BN;
     cudaError_t e =
-        cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mU, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, Cout_, um, isv, dN, BNr);
+        cudaLaunchKernelEx(&cfg, kern, mA, mAlo, mU, mX, M_, K_, NP_, Z_, cplx_, Mh_, kbh_, Cout_, um, isv, dN, BNr,
+                           PeerX{reinterpret_cast<const CUtensorMap *>(g.peer_maps), g.peer_col, g.npeer});
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
