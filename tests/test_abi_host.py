@@ -297,3 +297,20 @@ def test_fused_option_query():
         fc.plan_query(B, C, Co, x, x, 5, "winograd", 2, "auto", fused=1)
     with pytest.raises(fc.ConvError):  # out of range
         fc.plan_query(B, C, Co, x, x, 3, "winograd", 2, "auto", fused=2)
+
+
+def test_peer_exchange_arg_checks(lib):
+    """conv_eshard_forward_*_peer and conv_ipc_*: argument errors come back as statuses before any
+    device work (no GPU needed)."""
+    import ctypes
+    vp = ctypes.c_void_p
+    arr = (vp * 2)(None, None)
+    assert lib.conv_eshard_forward_a_peer(None, None, None, None, None, None, 0, None) == 1
+    assert lib.conv_eshard_forward_a_peer(None, None, None, arr, None, None, 0, None) == 1  # NULL plan
+    assert lib.conv_eshard_forward_b_peer(None, None, None, None, None, 0, None) == 1
+    p = vp()
+    h = (ctypes.c_char * 64)()
+    assert lib.conv_ipc_alloc(0, ctypes.byref(p), h) == 1
+    assert lib.conv_ipc_alloc(16, None, h) == 1
+    assert lib.conv_ipc_open(None, ctypes.byref(p)) == 1
+    assert lib.conv_ipc_free(None) == 0 and lib.conv_ipc_close(None) == 0  # NULL-safe
