@@ -13,7 +13,7 @@ using fct::cf;
 using namespace fcx;
 
 // ---------------------------------------------------------------- FFT NK2 ---
-constexpr int FTN = 32;  // tiles per CTA
+constexpr int FTN = 32;  // tiles per CTA (16 for grids of few CTAs, see launch_fft)
 
 template <int T>
 struct FftCfg {
@@ -21,7 +21,7 @@ struct FftCfg {
     static constexpr int S2 = (T * H) % 2 ? T * H : T * H + 1;  // odd stride (float2 units)
 };
 
-template <int T>
+template <int T, int FT = FTN>
 // flags: bit 0 channel-fastest grid, bit 1 tile rows 8-byte aligned (even W and m, aligned
 // input): float2 row loads, half the L1 requests of the lanes' scattered 4-byte loads.
 // 48 registers (5 CTAs/SM) for the composite t <= 16 codelets -- the kernel waits on its
@@ -30,12 +30,12 @@ template <int T>
 __global__ void __launch_bounds__(256, ((T <= 16 && T % 2 == 0) || T == 9) ? 5 : ((T <= 18) ? 4 : 0)) nk2_fft(Geometry g, const float *__restrict__ in, float *__restrict__ U,
                                                                  int flags) {
     constexpr int H = FftCfg<T>::H, S = FftCfg<T>::S2, RP = (T + 1) / 2;
-    extern __shared__ float2 zs[];  // [FTN][S]: tile nn, row a, bin l at nn*S + a*H + l
+    extern __shared__ float2 zs[];  // [FT][S]: tile nn, row a, bin l at nn*S + a*H + l
     const int cfast = flags & 1;
     const int c = cfast ? blockIdx.x : blockIdx.y;
-    const long long n0 = (long long)(cfast ? blockIdx.y : blockIdx.x) * FTN;
-    for (int it = threadIdx.x; it < RP * FTN; it += blockDim.x) {
-        const int nn = it % FTN, p = it / FTN;
+    const long long n0 = (long long)(cfast ? blockIdx.y : blockIdx.x) * FT;
+    for (int it = threadIdx.x; it < RP * FT; it += blockDim.x) {
+        const int nn = it % FT, p = it / FT;
         const int a0 = 2 * p, a1 = 2 * p + 1;
         const long long n = n0 + nn;
         cf z[T];
@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(256, ((T <= 16 && T % 2 == 0) || T == 9) ? 5 :
     }
     __syncthreads();
     float umx = 0.f;
-    for (int it = threadIdx.x; it < H * FTN; it += blockDim.x) {
-        const int nn = it % FTN, l = it / FTN;
+    for (int it = threadIdx.x; it < H * FT; it += blockDim.x) {
+        const int nn = it % FT, l = it / FT;
         const long long n = n0 + nn;
         cf z[T];
 #pragma unroll
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(256, ((T <= 16 && T % 2 == 0) || T == 9) ? 5 :
             }
         }
     }
-    if (g.umax) {  // per-image max|U|: a thread's items all have tile nn = threadIdx.x % FTN
-        const long long nt = n0 + (threadIdx.x % FTN);
+    if (g.umax) {  // per-image max|U|: a thread's items all have tile nn = threadIdx.x % FT
+        const long long nt = n0 + (threadIdx.x % FT);
         fc_block_umax_img(g.umax, fc_div((int)(n0 < g.BN ? n0 : g.BN - 1), g.divN),
                           nt < g.BN ? fc_div((int)nt, g.divN) : -1, umx);
     }
@@ -285,24 +285,36 @@ __global__ void __launch_bounds__(512, (T <= 18) ? 2 : 0) nk4_fft(Geometry g, in
 }
 
 
+template <int T, int FT>
+cudaError_t launch_nk2_fft(const Geometry &g, const float *src, float *dst, cudaStream_t s) {
+    constexpr int H = FftCfg<T>::H;
+    const unsigned nblk = (unsigned)((g.BN + FT - 1) / FT);
+    const size_t smem = sizeof(float2) * FT * FftCfg<T>::S2;
+    fc_smem_attr((const void *)nk2_fft<T, FT>, (int)smem);
+    // channel-fastest grid (measured faster); float2 row loads when tile rows are 8-byte aligned
+    const int v2 = (((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
+    // small tiles (t <= 12): CTAs of exactly max(row pairs, columns) x 32 threads -- one
+    // item each, no idle warps (VGG-3.2 t = 10 NK2 -7%, deep t = 9 -6%); larger tiles keep
+    // 256 (t = 16 at 288 threads: one CTA fewer per SM, VGG-1.2 m = 14 +5%)
+    constexpr int RPc = (T + 1) / 2, ITEMS = (RPc > H ? RPc : H) * FT;
+    const int nthr = (T <= 12 && ITEMS <= 256) ? (ITEMS + 31) / 32 * 32 : 256;
+    if (nblk <= 65535)
+        nk2_fft<T, FT><<<dim3(g.C, nblk), nthr, smem, s>>>(g, src, dst, 1 | v2);
+    else
+        nk2_fft<T, FT><<<dim3(nblk, g.C), nthr, smem, s>>>(g, src, dst, v2);
+    return cudaGetLastError();
+}
+
 template <int T>
 cudaError_t launch_fft(const Geometry &g, const float *src, float *dst, bool forward, cudaStream_t s) {
     constexpr int H = FftCfg<T>::H;
-    const unsigned nblk = (unsigned)((g.BN + FTN - 1) / FTN);
     if (forward) {
-        const size_t smem = sizeof(float2) * FTN * FftCfg<T>::S2;
-        fc_smem_attr((const void *)nk2_fft<T>, (int)smem);
-        // channel-fastest grid (measured faster); float2 row loads when tile rows are 8-byte aligned
-        const int v2 = (((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
-        // small tiles (t <= 12): CTAs of exactly max(row pairs, columns) x 32 threads -- one
-        // item each, no idle warps (VGG-3.2 t = 10 NK2 -7%, deep t = 9 -6%); larger tiles keep
-        // 256 (t = 16 at 288 threads: one CTA fewer per SM, VGG-1.2 m = 14 +5%)
-        constexpr int RPc = (T + 1) / 2, ITEMS = (RPc > H ? RPc : H) * FTN;
-        const int nthr = (T <= 12 && ITEMS <= 256) ? (ITEMS + 31) / 32 * 32 : 256;
-        if (nblk <= 65535)
-            nk2_fft<T><<<dim3(g.C, nblk), nthr, smem, s>>>(g, src, dst, 1 | v2);
-        else
-            nk2_fft<T><<<dim3(nblk, g.C), nthr, smem, s>>>(g, src, dst, v2);
+        // 16-tile CTAs when 32-tile ones would make fewer than 16 per SM over the whole grid
+        // (small layers: wave quantisation; 5x5 t = 18 NK2 64 -> 56 us); otherwise 32 tiles,
+        // each (z, channel) row of U a 128-byte run (VGG-1.2 t = 16 NK2 0.42 ms at 16 vs 0.37)
+        const long long ctas32 = (long long)g.C * ((g.BN + FTN - 1) / FTN);
+        if (ctas32 < 16LL * fc_num_sms()) return launch_nk2_fft<T, 16>(g, src, dst, s);
+        return launch_nk2_fft<T, FTN>(g, src, dst, s);
     } else {
         // tiles per CTA ~ 512 / H (one phase-A item per thread), shared memory <= ~100 KB;
         // whole images when they fit (IPC images), else strips of R tile rows
