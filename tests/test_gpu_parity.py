@@ -124,12 +124,17 @@ def _full_cases():
         for (method, m) in cfg.runs:
             for gemm in ("auto", "tcgen05"):
                 yield name, method, m, gemm
+        if cfg.r == 3:  # the fused NK2-NK4 F(2,3) kernel (conv_plan_options.fused) at full size
+            yield name, "winograd", 2, "fused"
 
 
 @pytest.mark.parametrize("name,method,m,gemm", list(_full_cases()))
 def test_full_size_full_tensor(name, method, m, gemm):
     cfg, I, W, Od, omax = _full(name)
-    p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm)  # bench.py's launch config
+    if gemm == "fused":
+        p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, "auto", fused=1)
+    else:
+        p = fc.Plan(cfg.B, cfg.C, cfg.Cout, cfg.H, cfg.W, cfg.r, method, m, gemm)  # bench.py's launch config
     y = p.forward(I.cuda(), W.cuda())
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
