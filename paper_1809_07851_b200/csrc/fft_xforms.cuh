@@ -293,11 +293,13 @@ cudaError_t launch_nk2_fft(const Geometry &g, const float *src, float *dst, cuda
     fc_smem_attr((const void *)nk2_fft<T, FT>, (int)smem);
     // channel-fastest grid (measured faster); float2 row loads when tile rows are 8-byte aligned
     const int v2 = (((g.W | g.m) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0) ? 2 : 0;
-    // small tiles (t <= 12): CTAs of exactly max(row pairs, columns) x 32 threads -- one
-    // item each, no idle warps (VGG-3.2 t = 10 NK2 -7%, deep t = 9 -6%); larger tiles keep
-    // 256 (t = 16 at 288 threads: one CTA fewer per SM, VGG-1.2 m = 14 +5%)
+    // small tiles (t <= 12) and the 16-tile CTAs of small grids: CTAs of exactly max(row
+    // pairs, columns) x 32 threads -- one item each, no idle warps (VGG-3.2 t = 10 NK2 -7%,
+    // deep t = 9 -6%; 5x5 t = 18 at 160 instead of 256 threads 66 -> 63.5 us, r02n A/B);
+    // larger 32-tile CTAs keep 256 (t = 16 at 288 threads: one CTA fewer per SM, VGG-1.2
+    // m = 14 +5%)
     constexpr int RPc = (T + 1) / 2, ITEMS = (RPc > H ? RPc : H) * FT;
-    const int nthr = (T <= 12 && ITEMS <= 256) ? (ITEMS + 31) / 32 * 32 : 256;
+    const int nthr = ((T <= 12 || FT < FTN) && ITEMS <= 256) ? (ITEMS + 31) / 32 * 32 : 256;
     if (nblk <= 65535)
         nk2_fft<T, FT><<<dim3(g.C, nblk), nthr, smem, s>>>(g, src, dst, 1 | v2);
     else
