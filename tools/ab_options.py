@@ -6,6 +6,7 @@ step, per-step CUDA events, median and min of 20 steps (not the bench contract l
         python tools/ab_options.py
 
 Each case is config:method:m:options, options "name=value" joined by ';' (empty: defaults).
+AB_LIB=expt/lib_x.so times an experiment build instead of the product library.
 """
 from __future__ import annotations
 
@@ -16,6 +17,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+if os.environ.get("AB_LIB"):  # an experiment build (tools/ab_stages.py) instead of the product library
+    from paper_1809_07851_b200 import _build
+    _build.LIB = os.path.abspath(os.environ["AB_LIB"])
 
 import torch  # noqa: E402
 
@@ -45,7 +50,8 @@ def main() -> None:
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        print(json.dumps({"case": "%s/%s/%s" % (name, method, m), "opts": opts,
+        print(json.dumps({"lib": os.path.basename(os.environ.get("AB_LIB", "product")),
+                          "case": "%s/%s/%s" % (name, method, m), "opts": opts,
                           "ms_median": round(statistics.median(ts), 4), "ms_min": round(min(ts), 4)}), flush=True)
         del p, ws, out, x, w
         torch.cuda.empty_cache()
